@@ -1,0 +1,962 @@
+// ouro_device.cuh -- in-kernel malloc/free for B200 (sm_100a), header-only.
+//
+//   #include "ouro_device.cuh"
+//   __global__ void k(ouro_heap_view h) { void* p = ouro_malloc(h, 1000); ... ouro_free(h, p); }
+//
+// Replaces the reference's alloc / dealloc / alloc_coalesced
+// for the six variants
+// {page, chunk} x {array, virtual-array, virtual-list} (config.hpp:55-69).
+// The protocol is the oracle's (oracle/ouro_oracle.cpp); this
+// file is its warp-aggregated CUDA form:
+//   * every call groups the converged lanes of a warp by size class
+//     (ballot/shfl on the leader's class), one leader does the count/ticket
+//     atomics for the whole group and broadcasts the ticket base with __shfl;
+//   * queue slots are 8-byte {tag, value} words read/written by each lane at
+//     ticket base + rank (coalesced: a warp touches 256 contiguous bytes);
+//   * chunk bitmaps are claimed cooperatively: each lane scans two 64-bit words
+//     (one 128-byte-coalesced pass over a 512 B bitmap), prefix sums by
+//     ballot, one fetch-AND per word;
+//   * frees aggregate by bitmap word (__match_any_sync + __reduce_or_sync) and
+//     by chunk, so a warp freeing 32 neighbouring pages does one fetch-OR and
+//     one free-count add.
+// Groups inside one warp are served in order of their lowest lane, ranks in
+// lane order, which makes a single-warp run deterministic and bit-identical to
+// the oracle's group operations.
+#ifndef OURO_DEVICE_CUH
+#define OURO_DEVICE_CUH
+
+#include <stdint.h>
+
+#include "ouro.h"
+#include "ouro/device_view.h"
+
+namespace ouro_dev {
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef long long i64;
+
+constexpr u32 NONE = 0xFFFFFFFFu;
+constexpr u64 NONE_LINK = ~0ull;
+constexpr u32 ST_UNASSIGNED = 0;
+constexpr u32 ST_RESERVED = 0xFF;
+constexpr int KIND_PAGE = OURO_KIND_PAGE;
+constexpr int KIND_CHUNK = OURO_KIND_CHUNK;
+constexpr int FL_ARRAY = OURO_FLAVOR_ARRAY;
+constexpr int FL_VA = OURO_FLAVOR_VIRTUAL_ARRAY;
+constexpr int FL_VL = OURO_FLAVOR_VIRTUAL_LIST;
+
+// ------------------------------------------------------------ primitives ----
+__device__ __forceinline__ u32 lane_id() { u32 r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
+__device__ __forceinline__ u32 lanemask_lt() { u32 r; asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r)); return r; }
+
+__device__ __forceinline__ u64 ld_rlx(const u64* p) {
+    u64 r; asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory"); return r;
+}
+__device__ __forceinline__ u64 ld_acq(const u64* p) {
+    u64 r; asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory"); return r;
+}
+__device__ __forceinline__ u32 ld_acq32(const u32* p) {
+    u32 r; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory"); return r;
+}
+__device__ __forceinline__ void ld_rlx_v2(const u64* p, u64& a, u64& b) {
+    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_rlx(u64* p, u64 v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_rel(u64* p, u64 v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_zero_v2(u64* p) {
+    asm volatile("st.global.v2.u64 [%0], {%1,%1};" :: "l"(p), "l"(0ull) : "memory");
+}
+__device__ __forceinline__ u64 shfl64(u32 mask, u64 v, u32 src) { return __shfl_sync(mask, v, src); }
+
+// exclusive prefix / total over the lanes of `mask` for values < 256
+__device__ __forceinline__ void ballot_scan8(u32 mask, u32 v, u32 lt, u32* pre, u32* tot) {
+    u32 p = 0, t = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const u32 bl = __ballot_sync(mask, (v >> b) & 1u);
+        p += (u32)__popc(bl & lt) << b;
+        t += (u32)__popc(bl) << b;
+    }
+    *pre = p;
+    *tot = t;
+}
+
+// the mask `todo` minus its `k` lowest set bits
+__device__ __forceinline__ u32 drop_lowest(u32 todo, u32 k) {
+    for (u32 i = 0; i < k && todo; ++i) todo &= todo - 1;
+    return todo;
+}
+
+__device__ __forceinline__ u32 nth_set64(u64 b, u32 x) {
+    for (u32 i = 0; i < x; ++i) b &= b - 1;
+    return (u32)(__ffsll((long long)b) - 1);
+}
+
+struct View {
+    const ouro_heap_view& v;
+    __device__ explicit View(const ouro_heap_view& x) : v(x) {}
+};
+
+__device__ __forceinline__ void raise_err(const ouro_heap_view& v, int code) {
+    atomicCAS(&v.sticky[0], 0u, (u32)code);
+    atomicOr(&v.sticky[1], 1u << code);
+    if (code == OURO_ERR_TIMEOUT) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_TIMEOUT], 1ull);
+    if (code == OURO_ERR_CORRUPTION) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_CORRUPTION], 1ull);
+}
+
+// Bounded spin: TimeoutError instead of a hung GPU.
+struct Spin {
+    u64 n = 0;
+    __device__ __forceinline__ bool step(const ouro_heap_view& v) {
+        ++n;
+        if (n > 16) __nanosleep(n < 4096 ? 32 : 256);
+        return n < v.spin_limit;
+    }
+};
+
+// backoff: FenceRetry = device fence; SleepRetry =
+// nanosleep(min(base * 2^attempt, cap)).
+__device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
+    if (v.backoff == OURO_BACKOFF_SLEEP) {
+        u64 ns = attempt >= 40 ? v.sleep_cap_ns : ((u64)v.sleep_base_ns << attempt);
+        if (ns > v.sleep_cap_ns) ns = v.sleep_cap_ns;
+        __nanosleep((u32)ns);
+    } else {
+        __threadfence();
+    }
+}
+
+// size_class_of; size 0 rejected like TooLarge (gap G5).
+__device__ __forceinline__ bool size_class(const ouro_heap_view& v, u64 req, u32* k) {
+    const u64 maxp = 1ull << (v.min_shift + v.K - 1);
+    if (req == 0 || req > maxp) return false;
+    const u32 lg = req <= 1 ? 0u : (u32)(64 - __clzll((long long)(req - 1)));
+    *k = lg > v.min_shift ? lg - v.min_shift : 0u;
+    return true;
+}
+
+__device__ __forceinline__ u32 m_free(u64 m) { return (u32)m; }
+__device__ __forceinline__ u32 m_state(u64 m) { return (u32)(m >> 32) & 0xFFu; }
+__device__ __forceinline__ u32 m_gen(u64 m) { return (u32)(m >> 40); }
+__device__ __forceinline__ u64 mk_meta(u32 gen, u32 state, u32 fr) {
+    return ((u64)(gen & 0xFFFFFFu) << 40) | ((u64)state << 32) | fr;
+}
+__device__ __forceinline__ u32 ppc_of(const ouro_heap_view& v, u32 k) { return (u32)(v.chunk_bytes >> (v.min_shift + k)); }
+__device__ __forceinline__ u32 words_of(const ouro_heap_view& v, u32 k) { return (ppc_of(v, k) + 63u) / 64u; }
+__device__ __forceinline__ u64* bm_row(const ouro_heap_view& v, u32 c) { return v.bitmap + (u64)c * v.Wmax; }
+__device__ __forceinline__ u64* chunk_words(const ouro_heap_view& v, u32 c) {
+    return reinterpret_cast<u64*>(v.base + ((u64)c << v.chunk_shift));
+}
+__device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) {
+    return v.chunk_bits >= 32 ? c : (c | ((gen & v.gmask) << v.chunk_bits));
+}
+
+// ------------------------------------------------------- count / tickets ----
+// Count reservation (broker-queue style).
+__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor) {
+    if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) return 0;  // pre-check, no RMW when empty
+    const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
+    const i64 avail = old - floor;
+    const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
+    if (got < n) atomicAdd((u64*)&Q->count, (u64)(n - got));
+    return got;
+}
+__device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
+    if ((i64)ld_rlx((const u64*)&Q->count) + (i64)n > (i64)Q->cap) return false;
+    const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)n);
+    if (old + (i64)n > (i64)Q->cap) { atomicAdd((u64*)&Q->count, (u64)(-(i64)n)); return false; }
+    return true;
+}
+
+__device__ __forceinline__ u32 vtag(u64 t) { return ((u32)t & 0x7FFFFFFFu) | 0x80000000u; }
+
+// ---------------------------------------------------------- Array slots ----
+// slot t&mask in round r = t>>shift: tag 2r empty, 2r+1 full.
+__device__ __forceinline__ bool arr_put(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32 val) {
+    u64* s = Q->slots + (t & Q->ring_mask);
+    const u32 r = (u32)(t >> Q->ring_shift);
+    Spin sp;
+    while ((u32)(ld_rlx(s) >> 32) != 2u * r)
+        if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+    st_rlx(s, ((u64)(2u * r + 1u) << 32) | val);
+    return true;
+}
+__device__ __forceinline__ bool arr_take(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32* val) {
+    u64* s = Q->slots + (t & Q->ring_mask);
+    const u32 r = (u32)(t >> Q->ring_shift);
+    Spin sp;
+    u64 x;
+    while ((u32)((x = ld_rlx(s)) >> 32) != 2u * r + 1u)
+        if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+    *val = (u32)x;
+    st_rlx(s, (u64)(2u * r + 2u) << 32);
+    return true;
+}
+
+// Warp-collective Array enqueue: lanes in `part` (all of one queue) enqueue
+// their value in lane order.  Called by every lane of `mask`.
+__device__ __forceinline__ bool arr_enqueue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
+                                            u32 lane, u32 part, u32 val) {
+    if (!part) return true;
+    const u32 leader = __ffs(part) - 1, n = __popc(part), rank = __popc(part & lanemask_lt());
+    u64 t0 = 0;
+    u32 ok = 0;
+    if (lane == leader) {
+        Spin sp;
+        while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
+            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        if (ok) t0 = atomicAdd((u64*)&Q->tail, (u64)n);
+    }
+    ok = __shfl_sync(mask, ok, leader);
+    t0 = shfl64(mask, t0, leader);
+    if (!ok) return false;
+    if ((part >> lane) & 1u) return arr_put(v, Q, t0 + rank, val);
+    return true;
+}
+
+// Warp-collective Array dequeue for the lanes of `todo`: returns how many were
+// served; the `got` lowest-ranked lanes of todo get *val (NONE on timeout).
+__device__ __forceinline__ u32 arr_dequeue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
+                                           u32 lane, u32 todo, i64 floor, u32* val) {
+    const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
+    u32 got = 0;
+    u64 t0 = 0;
+    if (lane == leader) {
+        got = reserve_deq(Q, n, floor);
+        if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
+    }
+    got = __shfl_sync(mask, got, leader);
+    t0 = shfl64(mask, t0, leader);
+    if (((todo >> lane) & 1u) && rank < got) {
+        if (!arr_take(v, Q, t0 + rank, val)) *val = NONE;
+    }
+    return got;
+}
+
+__device__ __forceinline__ void seg_count(ouro_queue_dev* Q, int d) {
+    if (d > 0) {
+        const u64 now = atomicAdd((u64*)&Q->seg_live, 1ull) + 1ull;
+        atomicMax((u64*)&Q->seg_hwm, now);
+    } else {
+        atomicAdd((u64*)&Q->seg_live, (u64)-1ll);
+    }
+}
+
+// Acquire one segment chunk from the queue's Array source for lane `who`,
+// then have every lane of `mask` zero it (16-byte stores).  Returns the chunk
+// (broadcast) or NONE after a timeout.
+__device__ __forceinline__ u32 seg_acquire_zero(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
+                                                u32 lane, u32 who) {
+    ouro_queue_dev* P = v.q + Q->seg_src;
+    u32 c = NONE;
+    Spin sp;
+    for (u32 attempt = 1;; ++attempt) {
+        const u32 got = arr_dequeue(v, P, mask, lane, 1u << who, 0, &c);
+        if (got) break;
+        u32 more = (lane == who) ? (sp.step(v) ? 1u : 0u) : 0u;
+        more = __shfl_sync(mask, more, who);
+        if (!more) { if (lane == who) raise_err(v, OURO_ERR_TIMEOUT); return NONE; }
+        backoff(v, attempt < 8 ? attempt : 8);
+    }
+    c = __shfl_sync(mask, c, who);
+    if (c == NONE) return NONE;
+    const u32 L = __popc(mask), li = __popc(mask & lanemask_lt());
+    u64* w = chunk_words(v, c);
+    const u64 nw = v.chunk_bytes / 8;
+    for (u64 i = 2ull * li; i < nw; i += 2ull * L) st_zero_v2(w + i);
+    __threadfence();
+    __syncwarp(mask);
+    return c;
+}
+
+// --------------------------------------------------------- VirtualArray ----
+__device__ __forceinline__ bool va_find(const ouro_heap_view& v, ouro_queue_dev* Q, u64 s, u32* c) {
+    u64* e = Q->dir + (s % Q->D);
+    Spin sp;
+    for (;;) {
+        const u64 x = ld_acq(e);
+        if ((u32)(x >> 32) == (u32)s && (u32)x != NONE) { *c = (u32)x; return true; }
+        if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+    }
+}
+__device__ __forceinline__ bool va_create(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
+                                          u32 who, u64 s) {
+    u64* e = Q->dir + (s % Q->D);
+    u32 ok = 1;
+    if (lane == who) {
+        const u64 want = ((u64)(u32)s << 32) | NONE;
+        Spin sp;
+        while (ld_acq(e) != want)
+            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); ok = 0; break; }
+    }
+    ok = __shfl_sync(mask, ok, who);
+    if (!ok) return false;
+    const u32 c = seg_acquire_zero(v, Q, mask, lane, who);
+    if (c == NONE) return false;
+    if (lane == who) {
+        atomicExch(Q->dcnt + (s % Q->D), 0u);
+        __threadfence();
+        st_rel(e, ((u64)(u32)s << 32) | c);
+        seg_count(Q, +1);
+    }
+    __syncwarp(mask);
+    return true;
+}
+
+// ---------------------------------------------------------- VirtualList ----
+__device__ __forceinline__ u32 lseq(u64 l) { return (u32)(l >> 32); }
+__device__ __forceinline__ u32 lchk(u64 l) { return (u32)l; }
+__device__ __forceinline__ u64 mklink(u64 s, u32 c) { return ((u64)(u32)s << 32) | c; }
+__device__ __forceinline__ u32* vl_counter(const ouro_heap_view& v, u32 c) {
+    return reinterpret_cast<u32*>(chunk_words(v, c) + 1);
+}
+
+__device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_dev* Q, u64 s, u32* out) {
+    Spin sp;
+    for (;;) {
+        const u64 tl = ld_acq(&Q->vl_tail);
+        if (lchk(tl) != NONE && lseq(tl) == (u32)s) { *out = lchk(tl); return true; }
+        const u64 h = ld_acq(&Q->vl_head);
+        if (lchk(h) != NONE) {
+            u32 i = lseq(h), cur = lchk(h);
+            if ((u32)((u32)s - i) >= 0x80000000u) { raise_err(v, OURO_ERR_CORRUPTION); return false; }
+            bool ok = true;
+            while (i != (u32)s) {
+                const u64 nx = ld_acq(chunk_words(v, cur));
+                if (ld_acq(&Q->vl_head) != h || nx == NONE_LINK) { ok = false; break; }
+                cur = lchk(nx);
+                ++i;
+            }
+            if (ok) { *out = cur; return true; }
+        }
+        if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+    }
+}
+__device__ __forceinline__ void vl_tail_max(ouro_queue_dev* Q, u64 l) {
+    u64 cur = ld_acq(&Q->vl_tail);
+    for (;;) {
+        if (lchk(cur) != NONE && (int)(lseq(l) - lseq(cur)) <= 0) return;
+        const u64 prev = atomicCAS((u64*)&Q->vl_tail, cur, l);
+        if (prev == cur) return;
+        cur = prev;
+    }
+}
+
+// Warp-collective: advance head over fully retired segments (counter ==
+// S'+1), returning each to the segment source in order.  `who` drives it.
+__device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
+                                               u32 lane, u32 who) {
+    const u32 full = (u32)v.S_vl + 1u;
+    for (;;) {
+        u32 go = 0, ch = NONE, released = 0;
+        if (lane == who) {
+            u64 h = ld_acq(&Q->vl_head);
+            ch = lchk(h);
+            if (ch != NONE && ld_acq32(vl_counter(v, ch)) == full) {
+                const u64 nx = ld_acq(chunk_words(v, ch));
+                if (nx != NONE_LINK) {
+                    go = 1;
+                    if (atomicCAS((u64*)&Q->vl_head, h, nx) == h) released = 1;
+                }
+            }
+        }
+        go = __shfl_sync(mask, go, who);
+        if (!go) return;
+        released = __shfl_sync(mask, released, who);
+        if (released) {
+            arr_enqueue(v, v.q + Q->seg_src, mask, lane, 1u << who, ch);
+            if (lane == who) seg_count(Q, -1);
+        }
+    }
+}
+// Warp-collective: lanes in `part` add `cnt` to segment `c`'s retire counter
+// (one lane per distinct segment); the lowest lane that completed one drives
+// the head advance.
+__device__ __forceinline__ void vl_add(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
+                                       bool part, u32 c, u32 cnt) {
+    u32 done = 0;
+    if (part) done = (atomicAdd(vl_counter(v, c), cnt) + cnt == (u32)v.S_vl + 1u) ? 1u : 0u;
+    const u32 dm = __ballot_sync(mask, done);
+    if (dm) vl_try_advance(v, Q, mask, lane, __ffs(dm) - 1);
+}
+__device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
+                                          u32 who, u64 s) {
+    const u32 c = seg_acquire_zero(v, Q, mask, lane, who);
+    if (c == NONE) return false;
+    u32 p = NONE, ok = 1;
+    if (lane == who) {
+        st_rlx(chunk_words(v, c), NONE_LINK);
+        __threadfence();
+        seg_count(Q, +1);
+        if (s == 0) {
+            st_rel(&Q->vl_head, mklink(0, c));
+            vl_tail_max(Q, mklink(0, c));
+        } else if (vl_locate(v, Q, s - 1, &p)) {
+            st_rel(chunk_words(v, p), mklink(s, c));
+            vl_tail_max(Q, mklink(s, c));
+        } else {
+            ok = 0;
+        }
+    }
+    ok = __shfl_sync(mask, ok, who);
+    p = __shfl_sync(mask, p, who);
+    if (!ok) return false;
+    if (s != 0) vl_add(v, Q, mask, lane, lane == who, p, 1u);  // link event
+    return true;
+}
+
+// ------------------------------------------------- flavour-generic queue ----
+template <int FL>
+__device__ __forceinline__ u64 seg_slots(const ouro_heap_view& v) { return FL == FL_VA ? v.S_va : v.S_vl; }
+
+template <int FL>
+__device__ __forceinline__ bool q_put(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32 val) {
+    if (FL == FL_ARRAY) return arr_put(v, Q, t, val);
+    u32 c;
+    u64 j;
+    if (FL == FL_VA) {
+        if (!va_find(v, Q, t / v.S_va, &c)) return false;
+        j = t % v.S_va;
+    } else {
+        if (!vl_locate(v, Q, t / v.S_vl, &c)) return false;
+        j = 2 + t % v.S_vl;
+    }
+    st_rlx(chunk_words(v, c) + j, ((u64)vtag(t) << 32) | val);
+    return true;
+}
+template <int FL>
+__device__ __forceinline__ bool q_take(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32* val, u32* segc) {
+    if (FL == FL_ARRAY) { *segc = NONE; return arr_take(v, Q, t, val); }
+    u32 c;
+    u64 j;
+    if (FL == FL_VA) {
+        if (!va_find(v, Q, t / v.S_va, &c)) return false;
+        j = t % v.S_va;
+    } else {
+        if (!vl_locate(v, Q, t / v.S_vl, &c)) return false;
+        j = 2 + t % v.S_vl;
+    }
+    u64* s = chunk_words(v, c) + j;
+    Spin sp;
+    u64 x;
+    while ((u32)((x = ld_rlx(s)) >> 32) != vtag(t))
+        if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+    *val = (u32)x;
+    *segc = c;
+    return true;
+}
+
+// Warp-collective enqueue of the lanes in `part` into queue `qi` (lane order).
+template <int FL>
+__device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 part, u32 val) {
+    ouro_queue_dev* Q = v.q + qi;
+    if (FL == FL_ARRAY) return arr_enqueue(v, Q, mask, lane, part, val);
+    if (!part) return true;
+    const u32 leader = __ffs(part) - 1, n = __popc(part), rank = __popc(part & lanemask_lt());
+    u64 t0 = 0;
+    u32 ok = 0;
+    if (lane == leader) {
+        Spin sp;
+        while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
+            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        if (ok) t0 = atomicAdd((u64*)&Q->tail, (u64)n);
+    }
+    ok = __shfl_sync(mask, ok, leader);
+    t0 = shfl64(mask, t0, leader);
+    if (!ok) return false;
+    const bool me = (part >> lane) & 1u;
+    const u64 t = t0 + rank;
+    const u64 S = seg_slots<FL>(v);
+    u32 creators = __ballot_sync(mask, me && (t % S) == 0);
+    bool good = true;
+    while (creators) {  // segment creations in ticket order, whole warp helps
+        const u32 cl = __ffs(creators) - 1;
+        const u64 s = shfl64(mask, t / S, cl);
+        const bool r = FL == FL_VA ? va_create(v, Q, mask, lane, cl, s) : vl_create(v, Q, mask, lane, cl, s);
+        good = good && r;
+        creators &= creators - 1;
+    }
+    if (me) good = q_put<FL>(v, Q, t, val) && good;
+    return good;
+}
+
+// Warp-collective dequeue for the lanes of `todo` (all on queue `qi`).
+template <int FL>
+__device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 todo,
+                                         i64 floor, u32* val) {
+    ouro_queue_dev* Q = v.q + qi;
+    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val);
+    const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
+    u32 got = 0;
+    u64 t0 = 0;
+    if (lane == leader) {
+        got = reserve_deq(Q, n, floor);
+        if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
+    }
+    got = __shfl_sync(mask, got, leader);
+    t0 = shfl64(mask, t0, leader);
+    if (!got) return 0;
+    const bool me = ((todo >> lane) & 1u) && rank < got;
+    const u64 t = t0 + rank;
+    u32 segc = NONE;
+    bool okt = false;
+    if (me) {
+        okt = q_take<FL>(v, Q, t, val, &segc);
+        if (!okt) *val = NONE;
+    }
+    // consumption bookkeeping per segment (one add per distinct segment)
+    const bool part = me && okt;
+    if (FL == FL_VA) {
+        const u64 s = t / v.S_va;
+        const u64 key = part ? s : (~0ull - lane);
+        const u32 grp = __match_any_sync(mask, key);
+        const u32 gl = __ffs(grp) - 1;
+        const u32 cnt = __popc(grp);
+        u32 retire = 0, rc = NONE;
+        if (part && lane == gl) {
+            if (atomicAdd(Q->dcnt + (s % Q->D), cnt) + cnt == (u32)v.S_va) {
+                retire = 1;
+                rc = (u32)ld_acq(Q->dir + (s % Q->D));
+            }
+        }
+        const u32 rm = __ballot_sync(mask, retire);
+        if (rm) {
+            arr_enqueue(v, v.q + Q->seg_src, mask, lane, rm, rc);
+            if (retire) {
+                __threadfence();
+                st_rel(Q->dir + (s % Q->D), ((u64)(u32)(s + Q->D) << 32) | NONE);
+                seg_count(Q, -1);
+            }
+        }
+    } else {
+        const u64 key = part ? (u64)segc : (~0ull - lane);
+        const u32 grp = __match_any_sync(mask, key);
+        const u32 gl = __ffs(grp) - 1;
+        vl_add(v, Q, mask, lane, part && lane == gl, segc, __popc(grp));
+    }
+    return got;
+}
+
+// Warp-collective: enqueue each participating lane's value into its own
+// queue qi, groups served in order of their lowest lane.
+template <int FL>
+__device__ __forceinline__ void q_enqueue_by_queue(const ouro_heap_view& v, u32 mask, u32 lane, bool part,
+                                                   u32 qi, u32 val) {
+    u32 pending = __ballot_sync(mask, part);
+    while (pending) {
+        const u32 leader = __ffs(pending) - 1;
+        const u32 gq = __shfl_sync(mask, qi, leader);
+        const u32 grp = __ballot_sync(mask, part && ((pending >> lane) & 1u) && qi == gq);
+        if (!q_enqueue<FL>(v, gq, mask, lane, grp, val) && ((grp >> lane) & 1u)) raise_err(v, OURO_ERR_CORRUPTION);
+        pending &= ~grp;
+    }
+}
+
+// ---------------------------------------------------------- chunk bitmap ----
+// Claim the `take` lowest set bits of chunk c's bitmap.
+// Each lane of `mask` scans two words per window; the requester of rank
+// `req` (< take, NONE for others) receives the req-th lowest claimed page.
+__device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k, u32 take, u32 mask,
+                                          u32 lane, u32 req) {
+    const u32 L = __popc(mask), lt = lanemask_lt(), li = __popc(mask & lt);
+    const u32 W = words_of(v, k);
+    u64* row = bm_row(v, c);
+    u32 claimed = 0, page = NONE;
+    Spin sp;
+    while (claimed < take) {
+        for (u32 wb = 0; wb < W && claimed < take; wb += 2 * L) {
+            const u32 wi = wb + 2 * li;
+            u64 w0 = 0, w1 = 0;
+            if (wi + 1 < W) {
+                if ((v.Wmax & 1u) == 0) ld_rlx_v2(row + wi, w0, w1);
+                else { w0 = ld_rlx(row + wi); w1 = ld_rlx(row + wi + 1); }
+            } else if (wi < W) {
+                w0 = ld_rlx(row + wi);
+            }
+            const u32 cnt = (u32)(__popcll((long long)w0) + __popcll((long long)w1));
+            u32 pre, tot;
+            ballot_scan8(mask, cnt, lt, &pre, &tot);
+            const u32 need = take - claimed;
+            u32 my = pre >= need ? 0u : min(cnt, need - pre);
+            u64 p0 = 0, p1 = 0;
+            for (u64 b = w0; my && b; b &= b - 1, --my) p0 |= b & (~b + 1);
+            for (u64 b = w1; my && b; b &= b - 1, --my) p1 |= b & (~b + 1);
+            u64 g0 = 0, g1 = 0;
+            if (p0) g0 = atomicAnd(row + wi, ~p0) & p0;
+            if (p1) g1 = atomicAnd(row + wi + 1, ~p1) & p1;
+            if (g0 != p0 || g1 != p1) raise_err(v, OURO_ERR_CORRUPTION);
+            const u32 gc = (u32)(__popcll((long long)g0) + __popcll((long long)g1));
+            u32 gpre, gtot;
+            ballot_scan8(mask, gc, lt, &gpre, &gtot);
+            u32 owners = __ballot_sync(mask, gc > 0);
+            while (owners) {
+                const u32 o = __ffs(owners) - 1;
+                const u64 ob0 = shfl64(mask, g0, o), ob1 = shfl64(mask, g1, o);
+                const u32 opre = __shfl_sync(mask, gpre, o), ow = __shfl_sync(mask, wi, o);
+                const u32 n0 = (u32)__popcll((long long)ob0);
+                const u32 ocnt = n0 + (u32)__popcll((long long)ob1);
+                if (req != NONE && req >= claimed + opre && req < claimed + opre + ocnt) {
+                    const u32 x = req - claimed - opre;
+                    page = x < n0 ? ow * 64 + nth_set64(ob0, x) : (ow + 1) * 64 + nth_set64(ob1, x - n0);
+                }
+                owners &= owners - 1;
+            }
+            claimed += gtot;
+        }
+        if (claimed < take) {
+            u32 more = sp.step(v) ? 1u : 0u;
+            more = __shfl_sync(mask, more, __ffs(mask) - 1);
+            if (!more) { if (lane == __ffs(mask) - 1) raise_err(v, OURO_ERR_TIMEOUT); break; }
+        }
+    }
+    return page;
+}
+
+// ------------------------------------------------------------ allocators ----
+// Page kind, class group `gm` (SPEC.md:258-262 + 335-339).
+template <int FL>
+__device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm, u32 mask, u32 lane,
+                                         void** res, int* st) {
+    u32 todo = gm, attempt = 0;
+    const u32 lt = lanemask_lt();
+    while (todo) {
+        const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
+        u32 h = NONE;
+        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h);
+        const bool mine = ((todo >> lane) & 1u) && rank < got;
+        bool ok = mine && h != NONE;
+        u32 c = 0, p = 0;
+        if (ok) {
+            c = h >> v.page_bits;
+            p = h & ((1u << v.page_bits) - 1u);
+        }
+        if (got) {
+            // clear the page bits, one fetch-AND per distinct word
+            u64* wp = bm_row(v, c) + (p >> 6);
+            const u64 bit = ok ? (1ull << (p & 63)) : 0ull;
+            const u32 grp = __match_any_sync(mask, ok ? (u64)wp : (~0ull - lane));
+            const u32 lo = __reduce_or_sync(grp, (u32)bit), hi = __reduce_or_sync(grp, (u32)(bit >> 32));
+            const u64 bits = ((u64)hi << 32) | lo;
+            const u32 gl = __ffs(grp) - 1;
+            if (ok && lane == gl) {
+                const u64 old = atomicAnd(wp, ~bits);
+                if ((old & bits) != bits) raise_err(v, OURO_ERR_CORRUPTION);
+            }
+            // free_count -= pages taken, one add per distinct chunk
+            const u32 cg = __match_any_sync(mask, ok ? (u64)c : (~0ull - lane));
+            if (ok && lane == __ffs(cg) - 1) atomicAdd(v.meta + c, (u64)(-(i64)__popc(cg)));
+            if (mine) {
+                if (ok) { *res = v.base + ((u64)c << v.chunk_shift) + ((u64)p << (v.min_shift + k)); *st = OURO_OK; }
+                else *st = OURO_ERR_TIMEOUT;
+            }
+        }
+        todo = drop_lowest(todo, got);
+        if (!todo) break;
+        if (lane == leader) atomicAdd(&v.ctr[k], (u64)__popc(todo));
+        if (++attempt >= v.max_retries) {
+            if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)__popc(todo));
+            if ((todo >> lane) & 1u) *st = OURO_ERR_OOM;
+            break;
+        }
+        backoff(v, attempt);
+        (void)n;
+    }
+}
+
+// Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).
+template <int FL>
+__device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm, u32 mask, u32 lane,
+                                         void** res, int* st) {
+    u32 todo = gm, attempt = 0;
+    const u32 lt = lanemask_lt();
+    const u32 ppc = ppc_of(v, k);
+    const u32 L = __popc(mask), li = __popc(mask & lt);
+    const u32 pool = v.K;
+    while (todo) {
+        const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
+        const bool intodo = (todo >> lane) & 1u;
+        u32 e = NONE;
+        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e);
+        e = __shfl_sync(mask, e, leader);
+        if (got && e != NONE) {
+            const u32 c = e & v.cmask;
+            const u32 glow = v.chunk_bits >= 32 ? 0u : (e >> v.chunk_bits);
+            u32 take = 0, oldfree = 0;
+            if (lane == leader) {
+                u64 m = ld_rlx(v.meta + c);
+                for (;;) {
+                    if (m_state(m) != k + 1 || (m_gen(m) & v.gmask) != glow || m_free(m) == 0) break;
+                    const u32 f = m_free(m);
+                    const u32 t = min(n, f);
+                    const u64 prev = atomicCAS(v.meta + c, m, m - t);
+                    if (prev == m) { take = t; oldfree = f; break; }
+                    m = prev;
+                }
+                if (!take) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_STALE], 1ull);
+            }
+            take = __shfl_sync(mask, take, leader);
+            oldfree = __shfl_sync(mask, oldfree, leader);
+            if (!take) continue;
+            const u32 page = warp_claim(v, c, k, take, mask, lane, (intodo && rank < take) ? rank : NONE);
+            q_enqueue<FL>(v, k, mask, lane, (oldfree - take > 0) ? (1u << leader) : 0u, e);  // in-transit rule
+            if (intodo && rank < take) {
+                if (page != NONE) {
+                    *res = v.base + ((u64)c << v.chunk_shift) + ((u64)page << (v.min_shift + k));
+                    *st = OURO_OK;
+                } else {
+                    *st = OURO_ERR_CORRUPTION;
+                }
+            }
+            todo = drop_lowest(todo, take);
+            continue;
+        }
+        u32 c = NONE;
+        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c);
+        c = __shfl_sync(mask, c, leader);
+        if (got && c != NONE) {
+            const u32 take = min(n, ppc);
+            u64 m = 0;
+            if (lane == leader) {
+                atomicAdd(&v.ctr[2 * v.K + OURO_CTR_POOL_DEQ], 1ull);
+                m = ld_rlx(v.meta + c);
+            }
+            m = shfl64(mask, m, leader);
+            if (m_state(m) != ST_UNASSIGNED) {
+                if (lane == leader) raise_err(v, OURO_ERR_CORRUPTION);
+                continue;
+            }
+            const u32 gen = (m_gen(m) + 1u) & 0xFFFFFFu;
+            // chunk_assign fused with taking pages 0..take-1 (whole warp writes the bitmap)
+            u64* row = bm_row(v, c);
+            const u32 W = words_of(v, k);
+            for (u32 w = li; w < W; w += L) {
+                const u32 lo = w * 64, hi = min(ppc, lo + 64);
+                u64 bits = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1ull);
+                const u32 th = min(take, hi);
+                if (th > lo) { const u32 nt = th - lo; bits &= (nt == 64) ? 0ull : ~((1ull << nt) - 1ull); }
+                st_rlx(row + w, bits);
+            }
+            __threadfence();
+            __syncwarp(mask);
+            if (lane == leader) {
+                st_rel(v.meta + c, mk_meta(gen, k + 1, ppc - take));
+                atomicAdd(v.assigned + k, 1u);
+            }
+            q_enqueue<FL>(v, k, mask, lane, (ppc - take > 0) ? (1u << leader) : 0u, q_entry(v, c, gen));
+            if (intodo && rank < take) {
+                *res = v.base + ((u64)c << v.chunk_shift) + ((u64)rank << (v.min_shift + k));
+                *st = OURO_OK;
+            }
+            todo = drop_lowest(todo, take);
+            continue;
+        }
+        if (lane == leader) atomicAdd(&v.ctr[k], (u64)n);
+        if (++attempt >= v.max_retries) {
+            if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)n);
+            if (intodo) *st = OURO_ERR_OOM;
+            break;
+        }
+        backoff(v, attempt);
+    }
+}
+
+// malloc for the converged lanes of the calling warp.
+template <int KIND, int FL>
+__device__ __forceinline__ void* malloc_impl(const ouro_heap_view& v, u64 bytes, int* status) {
+    const u32 mask = __activemask();
+    const u32 lane = lane_id();
+    u32 k = 0;
+    const bool valid = size_class(v, bytes, &k);
+    void* res = nullptr;
+    int st = valid ? OURO_ERR_OOM : OURO_ERR_TOO_LARGE;
+    const u32 bad = __ballot_sync(mask, !valid);
+    if (bad && lane == (u32)(__ffs(bad) - 1)) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_BAD_SIZE], (u64)__popc(bad));
+    u32 pending = __ballot_sync(mask, valid);
+    while (pending) {
+        const u32 leader = __ffs(pending) - 1;
+        const u32 gk = __shfl_sync(mask, k, leader);
+        const u32 gm = __ballot_sync(mask, valid && ((pending >> lane) & 1u) && k == gk);
+        if (KIND == KIND_PAGE) pq_alloc<FL>(v, gk, gm, mask, lane, &res, &st);
+        else cq_alloc<FL>(v, gk, gm, mask, lane, &res, &st);
+        pending &= ~gm;
+    }
+    if (status) *status = st;
+    return res;
+}
+
+// free for the converged lanes of the calling warp.
+template <int KIND, int FL>
+__device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr) {
+    const u32 mask = __activemask();
+    const u32 lane = lane_id();
+    const u32 lt = lanemask_lt();
+    int st = OURO_OK;
+    bool valid = false;
+    u32 c = 0, k = 0, pi = 0;
+    u64 off = 0;
+    if (ptr != nullptr) {
+        off = (u64)((uint8_t*)ptr - v.base);
+        if (off >= v.heap_bytes) {
+            st = OURO_ERR_INVALID_HANDLE;
+        } else {
+            c = (u32)(off >> v.chunk_shift);
+            const u32 s8 = m_state(ld_rlx(v.meta + c));
+            if (s8 == ST_UNASSIGNED || s8 == ST_RESERVED || s8 > v.K) {
+                st = OURO_ERR_INVALID_HANDLE;
+            } else {
+                k = s8 - 1;
+                const u64 in = off & (v.chunk_bytes - 1);
+                if (in & ((1ull << (v.min_shift + k)) - 1)) st = OURO_ERR_INVALID_HANDLE;
+                else { pi = (u32)(in >> (v.min_shift + k)); valid = true; }
+            }
+        }
+    }
+    // duplicates inside the group: all but the lowest lane are double frees
+    {
+        const u32 same = __match_any_sync(mask, valid ? off : (~0ull - lane));
+        if (valid && (same & lt)) { valid = false; st = OURO_ERR_DOUBLE_FREE; }
+    }
+    // set the page bits, one fetch-OR per distinct word (old bit set => DoubleFree)
+    {
+        u64* wp = bm_row(v, c) + (pi >> 6);
+        const u64 bit = valid ? (1ull << (pi & 63)) : 0ull;
+        const u32 grp = __match_any_sync(mask, valid ? (u64)wp : (~0ull - lane));
+        const u32 lo = __reduce_or_sync(grp, (u32)bit), hi = __reduce_or_sync(grp, (u32)(bit >> 32));
+        const u32 gl = __ffs(grp) - 1;
+        u64 old = 0;
+        if (valid && lane == gl) old = atomicOr(wp, ((u64)hi << 32) | lo);
+        old = shfl64(mask, old, gl);
+        if (valid && (old & bit)) { valid = false; st = OURO_ERR_DOUBLE_FREE; }
+    }
+    {
+        const u32 nd = __ballot_sync(mask, st == OURO_ERR_DOUBLE_FREE);
+        const u32 ni = __ballot_sync(mask, st == OURO_ERR_INVALID_HANDLE);
+        if (nd && lane == (u32)(__ffs(nd) - 1)) {
+            atomicAdd(&v.ctr[2 * v.K + OURO_CTR_DOUBLE_FREE], (u64)__popc(nd));
+            raise_err(v, OURO_ERR_DOUBLE_FREE);
+        }
+        if (ni && lane == (u32)(__ffs(ni) - 1)) {
+            atomicAdd(&v.ctr[2 * v.K + OURO_CTR_INVALID_FREE], (u64)__popc(ni));
+            raise_err(v, OURO_ERR_INVALID_HANDLE);
+        }
+    }
+    // free_count += pages released, one add per distinct chunk
+    const u32 cg = __match_any_sync(mask, valid ? (u64)c : (~0ull - lane));
+    const u32 cgl = __ffs(cg) - 1;
+    const bool cl = valid && lane == cgl;
+    u64 oldm = 0;
+    if (cl) oldm = atomicAdd(v.meta + c, (u64)__popc(cg));
+    const u32 oldfree = m_free(oldm), newfree = oldfree + (u32)__popc(cg), gen = m_gen(oldm);
+    if (KIND == KIND_CHUNK) {
+        const u32 ppc = ppc_of(v, k);
+        const bool closer = cl && newfree == ppc;
+        // watermark (gap G3): per class, min(#closers, assigned-1) may close
+        const u32 g2 = __match_any_sync(mask, closer ? (u64)k : (~0ull - lane));
+        const u32 g2l = __ffs(g2) - 1, r2 = __popc(g2 & lt);
+        u32 take = 0;
+        if (closer && lane == g2l) {
+            const u32 want = __popc(g2);
+            u32 cur = ld_acq32(v.assigned + k);
+            for (;;) {
+                take = cur > 1 ? min(want, cur - 1) : 0u;
+                if (!take) break;
+                const u32 prev = atomicCAS(v.assigned + k, cur, cur - take);
+                if (prev == cur) break;
+                cur = prev;
+            }
+        }
+        take = __shfl_sync(mask, take, g2l);
+        bool closed = false;
+        if (closer && r2 < take) {
+            const u64 expect = mk_meta(gen, k + 1, ppc);
+            if (atomicCAS(v.meta + c, expect, mk_meta(gen, ST_UNASSIGNED, 0)) == expect) closed = true;
+            else atomicAdd(v.assigned + k, 1u);
+        }
+        u32 cm = __ballot_sync(mask, closed);
+        if (cm) {
+            const u32 L = __popc(mask), li = __popc(mask & lt);
+            u32 it = cm;
+            while (it) {
+                const u32 o = __ffs(it) - 1;
+                const u32 oc = __shfl_sync(mask, c, o), ok_ = __shfl_sync(mask, k, o);
+                u64* row = bm_row(v, oc);
+                const u32 W = words_of(v, ok_);
+                for (u32 w = li; w < W; w += L) st_rlx(row + w, 0ull);
+                it &= it - 1;
+            }
+            __threadfence();
+            __syncwarp(mask);
+            arr_enqueue(v, v.q + v.K, mask, lane, cm, c);  // return to pool
+        }
+        // 0 -> >0: the releaser re-enqueues the chunk
+        q_enqueue_by_queue<FL>(v, mask, lane, cl && oldfree == 0 && !closed, k, q_entry(v, c, gen));
+    } else {
+        q_enqueue_by_queue<FL>(v, mask, lane, valid, k, (c << v.page_bits) | pi);
+    }
+    return st;
+}
+
+// all-or-nothing group allocation (alloc_coalesced)
+template <int KIND, int FL>
+__device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, u64 bytes, int* status) {
+    const u32 mask = __activemask();
+    int st;
+    void* p = malloc_impl<KIND, FL>(v, bytes, &st);
+    const u32 fails = __ballot_sync(mask, st != OURO_OK);
+    if (fails) {
+        const bool tl = __shfl_sync(mask, st, __ffs(mask) - 1) == OURO_ERR_TOO_LARGE;
+        if (p) free_impl<KIND, FL>(v, p);
+        __syncwarp(mask);
+        p = nullptr;
+        st = tl ? OURO_ERR_TOO_LARGE : OURO_ERR_OOM;
+    }
+    if (status) *status = st;
+    return p;
+}
+
+}  // namespace ouro_dev
+
+// ---------------------------------------------------------------- public ----
+// Compile-time variant entry points (fastest: no dispatch).
+template <int KIND, int FLAVOR>
+__device__ __forceinline__ void* ouro_malloc_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr) {
+    return ouro_dev::malloc_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status);
+}
+template <int KIND, int FLAVOR>
+__device__ __forceinline__ int ouro_free_t(const ouro_heap_view& h, void* p) {
+    return ouro_dev::free_impl<KIND, FLAVOR>(h, p);
+}
+template <int KIND, int FLAVOR>
+__device__ __forceinline__ void* ouro_malloc_coalesced_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr) {
+    return ouro_dev::malloc_coalesced_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status);
+}
+
+// Runtime-dispatched entry points (variant read from the view).
+#define OURO_DISPATCH(h, CALL)                                                            \
+    switch ((h).kind * 3 + (h).flavor) {                                                   \
+    case 0: CALL(0, 0); case 1: CALL(0, 1); case 2: CALL(0, 2);                            \
+    case 3: CALL(1, 0); case 4: CALL(1, 1); default: CALL(1, 2);                           \
+    }
+
+__device__ __noinline__ void* ouro_malloc(const ouro_heap_view& h, size_t bytes) {
+#define OURO_M(K, F) return ouro_malloc_t<K, F>(h, bytes)
+    OURO_DISPATCH(h, OURO_M)
+#undef OURO_M
+}
+__device__ __noinline__ void ouro_free(const ouro_heap_view& h, void* p) {
+#define OURO_F(K, F) ouro_free_t<K, F>(h, p); return
+    OURO_DISPATCH(h, OURO_F)
+#undef OURO_F
+}
+__device__ __noinline__ void* ouro_malloc_coalesced(const ouro_heap_view& h, size_t bytes) {
+#define OURO_C(K, F) return ouro_malloc_coalesced_t<K, F>(h, bytes)
+    OURO_DISPATCH(h, OURO_C)
+#undef OURO_C
+}
+
+#endif  // OURO_DEVICE_CUH

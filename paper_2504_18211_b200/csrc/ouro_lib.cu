@@ -1,0 +1,1164 @@
+// ouro_lib.cu -- libouro_b200: heap construction, driver-phase kernels and the
+// C-ABI of include/ouro.h (everything except the GPU-free config half, which is
+// ouro_config.cpp).  sm_100a only.
+//
+// The hot path itself is the header-only device allocator in
+// include/ouro_device.cuh; the kernels here are (a) the paper's driver phases
+// (alloc / write / verify / free) as batch
+// launchers, (b) construction (new_arena + allocator init, SPEC.md:45-53,
+// 244-251), (c) quiescent stats / canonical digest / disjointness audit
+// (SURVEY.md §8c), (d) mixed churn (BASELINE configs[3]),
+// (e) the single-warp op-script runner used for oracle parity, and (f) atomic
+// micro-benchmarks that give the roofline denominators.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <vector>
+
+#include "../../include/ouro.h"
+#include "../../include/ouro_device.cuh"
+#include "ouro_internal.h"
+
+using namespace ouro_dev;
+using ouro_host::Geometry;
+
+#define CK(x)                                                                          \
+    do {                                                                               \
+        cudaError_t e_ = (x);                                                          \
+        if (e_ != cudaSuccess) {                                                       \
+            std::fprintf(stderr, "ouro: %s failed: %s (%s:%d)\n", #x, cudaGetErrorString(e_), \
+                         __FILE__, __LINE__);                                          \
+            return OURO_ERR_CUDA;                                                      \
+        }                                                                              \
+    } while (0)
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__host__ __device__ inline u64 mix64h(u64 x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ inline u64 hmix(u64 a, u64 b) { return mix64h(a * 0x9E3779B97F4A7C15ull + mix64h(b)); }
+__host__ __device__ inline u64 pattern_base(u64 seed, u64 slot, u32 it) {
+    return mix64h(seed ^ (slot * 0xD1B54A32D192ED03ull) ^ ((u64)it * 0x8CB92BA72F3D8DD7ull));
+}
+__host__ __device__ inline u64 pattern_word(u64 base, u64 w) { return base ^ (w * 0x9E3779B97F4A7C15ull) ^ (w << 7); }
+
+u64 next_pow2(u64 v) { return v <= 1 ? 1 : (1ull << (64 - __builtin_clzll(v - 1))); }
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+unsigned grid_for(u64 n) { return (unsigned)std::max<u64>(1, (n + kBlock - 1) / kBlock); }
+
+// ----------------------------------------------------------- construction ----
+__global__ void k_fill_ring(u64* slots, u64 R, u64 cap, int mode, u32 first_chunk, u32 ppc, u32 page_bits) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < R; t += (u64)gridDim.x * blockDim.x) {
+        u64 v = 0;
+        if (t < cap) {
+            u32 val;
+            if (mode == 0) val = (u32)t;
+            else val = ((first_chunk + (u32)(t / ppc)) << page_bits) | (u32)(t % ppc);
+            v = (1ull << 32) | val;
+        }
+        slots[t] = v;
+    }
+}
+
+// Prefill a virtual queue's first segments (consecutive chunks from `seg0`).
+__global__ void k_fill_segments(uint8_t* heap, u32 chunk_shift, u32 seg0, u64 S, u32 hdr, u64 cap,
+                                u32 first_chunk, u32 ppc, u32 page_bits) {
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t < cap; t += (u64)gridDim.x * blockDim.x) {
+        const u32 c = seg0 + (u32)(t / S);
+        u64* w = reinterpret_cast<u64*>(heap + ((u64)c << chunk_shift));
+        const u32 val = ((first_chunk + (u32)(t / ppc)) << page_bits) | (u32)(t % ppc);
+        w[hdr + t % S] = ((u64)vtag(t) << 32) | val;
+    }
+}
+__global__ void k_vl_headers(uint8_t* heap, u32 chunk_shift, u32 seg0, u32 m) {
+    const u32 i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    u64* w = reinterpret_cast<u64*>(heap + ((u64)(seg0 + i) << chunk_shift));
+    w[0] = (i + 1 < m) ? (((u64)(i + 1) << 32) | (seg0 + i + 1)) : NONE_LINK;
+    w[1] = (i + 1 < m) ? 1ull : 0ull;
+}
+// Page-kind chunk headers: Reserved segment storage or Assigned(k) fully free.
+__global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
+    const u32 c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= v.N) return;
+    const u32* start = pq;
+    const u32* n = pq + v.K;
+    const u32* s = pq + 2 * v.K;
+    u32 k = 0;
+    while (k + 1 < v.K && c >= start[k] + n[k]) ++k;
+    u64* row = bm_row(v, c);
+    if (c - start[k] < s[k]) {
+        v.meta[c] = mk_meta(0, ST_RESERVED, 0);
+        return;
+    }
+    const u32 ppc = ppc_of(v, k);
+    v.meta[c] = mk_meta(1, k + 1, ppc);
+    for (u32 w = 0; w < words_of(v, k); ++w) {
+        const u32 lo = w * 64, hi = min(ppc, lo + 64);
+        row[w] = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1ull);
+    }
+}
+
+// ------------------------------------------------------------ driver phases ----
+template <int KIND, int FL>
+__global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const u32* sizes, void** out) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const u64 sz = sizes ? sizes[i] : uniform;
+    out[i] = ouro_malloc_t<KIND, FL>(v, sz);
+}
+template <int KIND, int FL>
+__global__ void __launch_bounds__(kBlock) k_free(ouro_heap_view v, u64 n, void* const* ptrs) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    ouro_free_t<KIND, FL>(v, ptrs[i]);
+}
+
+__device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p) {
+    const u64 off = (u64)((const uint8_t*)p - v.base);
+    const u32 st = m_state(v.meta[off >> v.chunk_shift]);
+    if (st == 0 || st > v.K) return 0;
+    return 1ull << (v.min_shift + st - 1);
+}
+
+// Pattern writer / verifier.  Regions of >= 512 B are
+// processed by the whole warp (16 B per lane per store, coalesced); smaller
+// ones by their own thread.
+template <bool VERIFY>
+__global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, void* const* ptrs, u64 seed, u32 it,
+                                                    u64* result) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u32 lane = threadIdx.x & 31;
+    void* p = i < n ? ptrs[i] : nullptr;
+    const u64 len = p ? region_len(v, p) : 0;
+    u64 bad = 0;
+    const u32 big = __ballot_sync(0xFFFFFFFFu, len >= 512);
+    if (len && len < 512) {
+        const u64 b = pattern_base(seed, i, it);
+        u64* w = reinterpret_cast<u64*>(p);
+        for (u64 j = 0; j < len / 8; j += 2) {
+            if (VERIFY) {
+                const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
+                bad += (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
+            } else {
+                reinterpret_cast<ulonglong2*>(w)[j / 2] = make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+            }
+        }
+    }
+    u32 it_mask = big;
+    while (it_mask) {
+        const u32 src = __ffs(it_mask) - 1;
+        u64* w = reinterpret_cast<u64*>(__shfl_sync(0xFFFFFFFFu, (u64)p, src));
+        const u64 L = __shfl_sync(0xFFFFFFFFu, len, src);
+        const u64 slot = i - lane + src;
+        const u64 b = pattern_base(seed, slot, it);
+        for (u64 j = 2 * lane; j < L / 8; j += 64) {
+            if (VERIFY) {
+                const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
+                const u64 nb = (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
+                if (nb) { bad += nb; atomicMin(&result[1], slot); }
+            } else {
+                reinterpret_cast<ulonglong2*>(w)[j / 2] = make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+            }
+        }
+        it_mask &= it_mask - 1;
+    }
+    if (VERIFY) {
+        if (bad && len && len < 512) atomicMin(&result[1], i);
+        for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
+        if (lane == 0 && bad) atomicAdd(&result[0], bad);
+    }
+}
+
+__global__ void k_count(u64 n, void* const* ptrs, u64* count) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const bool live = i < n && ptrs[i] != nullptr;
+    const u32 b = __ballot_sync(0xFFFFFFFFu, live);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (u64)__popc(b));
+}
+
+// ------------------------------------------------------------------- audit ----
+__global__ void k_audit_collect(ouro_heap_view v, u64 n, void* const* ptrs, u64* offs, u64* lens, u64* res,
+                                unsigned long long* idx) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (i >= n || !ptrs[i]) return;
+    const u64 off = (u64)((uint8_t*)ptrs[i] - v.base);
+    atomicAdd(&res[0], 1ull);
+    if (off >= v.heap_bytes) { atomicAdd(&res[1], 1ull); return; }
+    const u32 c = (u32)(off >> v.chunk_shift);
+    const u32 st = m_state(v.meta[c]);
+    if (st == 0 || st > v.K) { atomicAdd(&res[1], 1ull); return; }
+    const u32 k = st - 1;
+    const u64 len = 1ull << (v.min_shift + k);
+    if (off & (len - 1)) atomicAdd(&res[2], 1ull);
+    const u32 p = (u32)((off & (v.chunk_bytes - 1)) >> (v.min_shift + k));
+    if ((bm_row(v, c)[p >> 6] >> (p & 63)) & 1ull) atomicAdd(&res[4], 1ull);
+    atomicAdd(&res[5], len);
+    const u64 j = atomicAdd(idx, 1ull);
+    offs[j] = off;
+    lens[j] = len;
+}
+__global__ void k_audit_neighbours(u64 m, const u64* offs, const u64* lens, u64* res) {
+    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (i + 1 >= m) return;
+    if (offs[i] + lens[i] > offs[i + 1]) atomicAdd(&res[3], 1ull);
+}
+
+// ------------------------------------------------------------------- churn ----
+template <int KIND, int FL>
+__global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
+                                                  uint8_t* touched, u64* res) {
+    const u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const u64 h = mix64h(seed ^ (t << 32) ^ r);
+    void* s = slots[t];
+    u32 ev_ok = 0, ev_fail = 0, ev_free = 0, ev_reuse = 0, ev_bad = 0;
+    if (s && (h & 1)) {
+        ouro_free_t<KIND, FL>(v, s);
+        slots[t] = nullptr;
+        ev_free = 1;
+    } else if (!s) {
+        void* p = ouro_malloc_t<KIND, FL>(v, 8 + (h >> 1) % 4089);
+        if (p) {
+            *reinterpret_cast<u64*>(p) = mix64h(t ^ seed);
+            slots[t] = p;
+            ev_ok = 1;
+            const u64 g = (u64)((uint8_t*)p - v.base) >> v.min_shift;
+            const u32 old = atomicOr(reinterpret_cast<u32*>(touched) + (g >> 5), 1u << (g & 31));
+            ev_reuse = (old >> (g & 31)) & 1u;
+        } else {
+            ev_fail = 1;
+        }
+    } else {
+        ev_bad = *reinterpret_cast<const u64*>(s) != mix64h(t ^ seed);
+    }
+    const u32 m = __activemask();
+    const u32 lane = lane_id();
+    const u32 a = __ballot_sync(m, ev_ok), b = __ballot_sync(m, ev_fail), c = __ballot_sync(m, ev_free);
+    const u32 d = __ballot_sync(m, ev_reuse), e = __ballot_sync(m, ev_bad);
+    if (lane == (u32)(__ffs(m) - 1)) {
+        if (a) atomicAdd(&res[0], (u64)__popc(a));
+        if (b) atomicAdd(&res[1], (u64)__popc(b));
+        if (c) atomicAdd(&res[2], (u64)__popc(c));
+        if (d) atomicAdd(&res[3], (u64)__popc(d));
+        if (e) atomicAdd(&res[4], (u64)__popc(e));
+    }
+}
+
+// --------------------------------------------------------- op-script runner ----
+template <int KIND, int FL>
+__global__ void k_script(ouro_heap_view v, const ouro_script_step* steps, u32 nsteps, u64* out_off, int* out_st) {
+    const u32 lane = threadIdx.x;
+    for (u32 s = 0; s < nsteps; ++s) {
+        const ouro_script_step& st = steps[s];
+        out_off[s * 32 + lane] = ~0ull;
+        out_st[s * 32 + lane] = -1;
+        __syncwarp();
+        if ((st.lane_mask >> lane) & 1u) {
+            if (st.op == 0 || st.op == 2) {
+                int status;
+                void* p = st.op == 0 ? ouro_malloc_t<KIND, FL>(v, st.arg[lane], &status)
+                                     : ouro_malloc_coalesced_t<KIND, FL>(v, st.arg[lane], &status);
+                out_off[s * 32 + lane] = p ? (u64)((uint8_t*)p - v.base) : ~0ull;
+                out_st[s * 32 + lane] = status;
+            } else {
+                const u64 a = st.arg[lane];
+                u64 off;
+                if (a >> 63) off = a & ~(1ull << 63);
+                else off = a < (u64)s * 32 ? out_off[a] : ~0ull;
+                if (off == ~0ull) off = ~1ull;
+                out_st[s * 32 + lane] = ouro_free_t<KIND, FL>(v, v.base + off);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// --------------------------------------------------------------- digest ----
+struct DigestDev {
+    u64 header_hash;
+    u64 queue_hash;
+    u64 live_pages;
+    u64 assigned_total;
+    u32 bad;
+    u32 pad;
+    u64 class_chunks[OURO_MAX_CLASSES];
+    u64 class_queued_live[OURO_MAX_CLASSES];
+    u64 class_live_pages[OURO_MAX_CLASSES];
+};
+
+__global__ void k_digest_headers(ouro_heap_view v, DigestDev* d, u32* where) {
+    const u32 c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= v.N) return;
+    const u64 m = v.meta[c];
+    const u32 st = m_state(m);
+    const u64* b = bm_row(v, c);
+    u64 bh = 0, pc = 0, any = 0;
+    for (u32 w = 0; w < v.Wmax; ++w) {
+        bh = hmix(bh ^ w, b[w]);
+        pc += __popcll(b[w]);
+        any |= b[w];
+    }
+    atomicAdd(&d->header_hash, v.kind == OURO_KIND_PAGE ? hmix(hmix(c, m), bh) : hmix(m & 0xFFFFFFFFFFull, bh));
+    if (st == ST_RESERVED) return;
+    if (st == ST_UNASSIGNED) {
+        if (m_free(m) != 0 || any) atomicOr(&d->bad, 1u);
+        return;
+    }
+    if (st > v.K) { atomicOr(&d->bad, 2u); return; }
+    const u32 k = st - 1;
+    atomicAdd(where + c, 1u);
+    atomicAdd(&d->assigned_total, 1ull);
+    atomicAdd(&d->class_chunks[k], 1ull);
+    const u64 live = ppc_of(v, k) - m_free(m);
+    atomicAdd(&d->class_live_pages[k], live);
+    atomicAdd(&d->live_pages, live);
+    if (pc != m_free(m)) atomicOr(&d->bad, 4u);
+}
+
+// Value of ticket t in a quiescent queue (segment table for virtual flavours).
+__device__ __forceinline__ bool ticket_value(const ouro_heap_view& v, const ouro_queue_dev& Q, const u32* segtab,
+                                             u64 seg_first, u64 t, u32* out) {
+    u64 x;
+    if (Q.flavor == FL_ARRAY) {
+        x = Q.slots[t & Q.ring_mask];
+    } else {
+        const u64 S = Q.flavor == FL_VA ? v.S_va : v.S_vl;
+        const u64 s = t / S;
+        const u32 c = segtab[s - seg_first];
+        if (c == NONE) return false;
+        x = chunk_words(v, c)[(Q.flavor == FL_VA ? 0 : 2) + t % S];
+    }
+    *out = (u32)x;
+    return true;
+}
+
+// mode 0: pool / private pool (where[c]++), 1: page-kind class k, 2: chunk-kind class k
+__global__ void k_digest_queue(ouro_heap_view v, const ouro_queue_dev* Qp, const u32* segtab, u64 seg_first, int mode,
+                               u32 k, DigestDev* d, u32* where, u32* entries) {
+    const ouro_queue_dev& Q = *Qp;
+    const u64 n = Q.tail - Q.head;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u32 x;
+        if (!ticket_value(v, Q, segtab, seg_first, Q.head + i, &x)) { atomicOr(&d->bad, 8u); continue; }
+        if (mode == 0) {
+            if (x < v.N) atomicAdd(where + x, 1u);
+            else atomicOr(&d->bad, 16u);
+        } else if (mode == 1) {
+            atomicAdd(&d->queue_hash, hmix(k + 1, x));
+            atomicAdd(&d->class_queued_live[k], 1ull);
+        } else {
+            const u32 c = x & v.cmask;
+            const u32 glow = v.chunk_bits >= 32 ? 0u : x >> v.chunk_bits;
+            const u64 m = v.meta[c];
+            if (m_state(m) == k + 1 && (m_gen(m) & v.gmask) == glow) {
+                atomicAdd(entries + c, 1u);
+                atomicAdd(&d->class_queued_live[k], 1ull);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------- atomic peaks ----
+__global__ void k_atom_distinct32(u32* a, u64 words, u32 iters) {
+    const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    u32 acc = 0;
+    for (u32 r = 0; r < iters; ++r) {
+        const u64 idx = ((tid + r * stride) * 8) % words;  // one 4 B counter per 32 B sector
+        acc += atomicAdd(a + idx, 1u);
+    }
+    if (acc == 0xFFFFFFFFu) a[0] = acc;
+}
+__global__ void k_atom_distinct_cas64(u64* a, u64 words, u32 iters) {
+    const u64 tid = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    u64 acc = 0;
+    for (u32 r = 0; r < iters; ++r) {
+        const u64 idx = ((tid + r * stride) * 4) % words;
+        const u64 old = a[idx];
+        acc += atomicCAS(a + idx, old, old + 1);
+    }
+    if (acc == ~0ull) a[0] = acc;
+}
+__global__ void k_atom_same_warp(u64* a, u32 iters) {
+    u64 acc = 0;
+    for (u32 r = 0; r < iters; ++r) {
+        u64 x = 0;
+        if ((threadIdx.x & 31) == 0) x = atomicAdd(a, 1ull);
+        acc += __shfl_sync(0xFFFFFFFFu, x, 0);
+    }
+    if (acc == ~0ull) a[1] = acc;
+}
+__global__ void k_atom_same_lane(u64* a, u32 iters) {
+    u64 acc = 0;
+    for (u32 r = 0; r < iters; ++r) {
+        u64 x;
+        asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(x) : "l"(a), "l"((u64)(threadIdx.x + r)) : "memory");
+        acc += x;
+    }
+    if (acc == ~0ull) a[1] = acc;
+}
+
+// ------------------------------------------------------------ variant switch ----
+#define OURO_VSWITCH(H, FN, ...)                                            \
+    switch ((H)->cfg.allocator_kind * 3 + (H)->cfg.queue_flavor) {          \
+    case 0: FN<0, 0>(__VA_ARGS__); break;                                   \
+    case 1: FN<0, 1>(__VA_ARGS__); break;                                   \
+    case 2: FN<0, 2>(__VA_ARGS__); break;                                   \
+    case 3: FN<1, 0>(__VA_ARGS__); break;                                   \
+    case 4: FN<1, 1>(__VA_ARGS__); break;                                   \
+    default: FN<1, 2>(__VA_ARGS__); break;                                  \
+    }
+
+template <int K, int F>
+void launch_alloc(ouro_heap* H, u64 n, u64 uni, const u32* sizes, void** out, cudaStream_t st) {
+    k_alloc<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, uni, sizes, out);
+}
+template <int K, int F>
+void launch_free(ouro_heap* H, u64 n, void* const* p, cudaStream_t st) {
+    k_free<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, p);
+}
+template <int K, int F>
+void launch_churn(ouro_heap* H, u64 n, u32 r, u64 seed, void** slots, u64* res, cudaStream_t st) {
+    k_churn<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, r, seed, slots, H->d_touched, res);
+}
+template <int K, int F>
+void launch_script(ouro_heap* H, const ouro_script_step* s, u32 n, u64* o, int* st) {
+    k_script<K, F><<<1, 32>>>(H->view, s, n, o, st);
+}
+
+// ---------------------------------------------------------- heap building ----
+void* dalloc(ouro_heap* H, size_t bytes) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+    H->owned.push_back(p);
+    return p;
+}
+
+// Allocate every device structure once (sizes depend only on the config).
+ouro_status plan(ouro_heap* H) {
+    const Geometry& g = H->g;
+    const u32 N = g.N, K = g.K;
+    H->nq = 2 * K + 1;
+    H->hq.assign(H->nq, ouro_queue_dev{});
+    H->pq_start.assign(K, 0);
+    H->pq_n.assign(K, 0);
+    H->pq_s.assign(K, 0);
+    const u64 S_va = g.chunk / 8, S_vl = g.chunk / 8 - 2;
+    auto init_q = [&](ouro_queue_dev& q, u32 flavor, u64 cap, int seg_src) -> bool {
+        q.flavor = flavor;
+        q.cap = cap;
+        q.seg_src = seg_src;
+        if (flavor == FL_ARRAY) {
+            const u64 R = next_pow2(std::max<u64>(cap, 1));
+            q.ring_shift = (u32)__builtin_ctzll(R);
+            q.ring_mask = R - 1;
+            q.slots = static_cast<u64*>(dalloc(H, R * 8));
+            return q.slots != nullptr;
+        }
+        if (flavor == FL_VA) {
+            q.D = (u32)((cap + S_va - 1) / S_va + 2);
+            q.dir = static_cast<u64*>(dalloc(H, (size_t)q.D * 8));
+            q.dcnt = static_cast<u32*>(dalloc(H, (size_t)q.D * 4));
+            return q.dir && q.dcnt;
+        }
+        return true;
+    };
+    const u32 fl = H->cfg.queue_flavor;
+    if (H->cfg.allocator_kind == OURO_KIND_PAGE) {
+        u32 at = 0;
+        for (u32 k = 0; k < K; ++k) {
+            H->pq_n[k] = N / K + (k == 0 ? N % K : 0);
+            H->pq_start[k] = at;
+            at += H->pq_n[k];
+        }
+        for (u32 k = 0; k < K; ++k) {
+            const u64 ppc = g.ppc(k);
+            u32 s = 0;
+            if (fl != FL_ARRAY) {  // gap G1: self-hosted segment reserve
+                const u64 Sx = fl == FL_VA ? S_va : S_vl;
+                for (s = 0; s <= H->pq_n[k]; ++s) {
+                    const u64 cap = (u64)(H->pq_n[k] - s) * ppc;
+                    const u64 need = cap == 0 ? 0 : (cap + Sx - 1) / Sx + 2;
+                    if (need <= s) break;
+                }
+            }
+            H->pq_s[k] = s;
+            const u64 cap = (u64)(H->pq_n[k] - s) * ppc;
+            if (fl == FL_ARRAY) {
+                if (!init_q(H->hq[k], FL_ARRAY, cap, -1)) return OURO_ERR_CUDA;
+            } else {
+                if (!init_q(H->hq[K + 1 + k], FL_ARRAY, std::max<u32>(s, 1), -1)) return OURO_ERR_CUDA;
+                if (!init_q(H->hq[k], fl, cap, (int)(K + 1 + k))) return OURO_ERR_CUDA;
+            }
+        }
+        if (!init_q(H->hq[K], FL_ARRAY, 1, -1)) return OURO_ERR_CUDA;
+        H->d_pq = static_cast<u32*>(dalloc(H, 3 * K * 4));
+        if (!H->d_pq) return OURO_ERR_CUDA;
+    } else {
+        if (!init_q(H->hq[K], FL_ARRAY, N, -1)) return OURO_ERR_CUDA;
+        for (u32 k = 0; k < K; ++k)
+            if (!init_q(H->hq[k], fl, 2ull * N, (int)K)) return OURO_ERR_CUDA;
+        H->floor_F = fl == FL_ARRAY ? 0 : (int64_t)std::min<u32>(K, N / 8);
+    }
+    return OURO_OK;
+}
+
+// (Re)initialise all contents: freshly constructed heap.
+ouro_status fill(ouro_heap* H, cudaStream_t st) {
+    const Geometry& g = H->g;
+    const u32 N = g.N, K = g.K;
+    const u32 fl = H->cfg.queue_flavor;
+    const u64 S_va = g.chunk / 8, S_vl = g.chunk / 8 - 2;
+    CK(cudaMemsetAsync(H->d_meta, 0, (size_t)N * 8, st));
+    CK(cudaMemsetAsync(H->d_bitmap, 0, (size_t)N * g.Wmax * 8, st));
+    CK(cudaMemsetAsync(H->d_assigned, 0, (size_t)K * 4, st));
+    CK(cudaMemsetAsync(H->d_ctr, 0, (size_t)(2 * K + OURO_CTR_N) * 8, st));
+    CK(cudaMemsetAsync(H->d_sticky, 0, 8, st));
+    if (H->d_touched) CK(cudaMemsetAsync(H->d_touched, 0, g.heap / g.minp / 8 + 8, st));
+    for (auto& q : H->hq) {
+        q.count = 0; q.head = 0; q.tail = 0; q.seg_live = 0; q.seg_hwm = 0;
+        q.vl_head = q.vl_tail = ((u64)0 << 32) | NONE;
+    }
+    auto ring_fill = [&](ouro_queue_dev& q, u64 cap, int mode, u32 first, u32 ppc) -> ouro_status {
+        const u64 R = q.ring_mask + 1;
+        k_fill_ring<<<std::min<u64>((R + kBlock - 1) / kBlock, 148 * 64), kBlock, 0, st>>>(q.slots, R, cap, mode, first, ppc, g.page_bits);
+        CK(cudaGetLastError());
+        q.count = (int64_t)cap;
+        q.tail = cap;
+        return OURO_OK;
+    };
+    auto dir_init = [&](ouro_queue_dev& q, u32 m, u32 seg0) -> ouro_status {
+        std::vector<u64> dir(q.D);
+        for (u32 i = 0; i < q.D; ++i) dir[i] = ((u64)i << 32) | (i < m ? seg0 + i : NONE);
+        CK(cudaMemcpyAsync(q.dir, dir.data(), (size_t)q.D * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(q.dcnt, 0, (size_t)q.D * 4, st));
+        CK(cudaStreamSynchronize(st));
+        return OURO_OK;
+    };
+    if (H->cfg.allocator_kind == OURO_KIND_PAGE) {
+        std::vector<u32> pq(3 * K);
+        for (u32 k = 0; k < K; ++k) { pq[k] = H->pq_start[k]; pq[K + k] = H->pq_n[k]; pq[2 * K + k] = H->pq_s[k]; }
+        CK(cudaMemcpyAsync(H->d_pq, pq.data(), 3 * K * 4, cudaMemcpyHostToDevice, st));
+        k_init_pq_chunks<<<grid_for(N), kBlock, 0, st>>>(H->view, H->d_pq);
+        CK(cudaGetLastError());
+        for (u32 k = 0; k < K; ++k) {
+            const u32 ppc = g.ppc(k);
+            const u32 s = H->pq_s[k];
+            const u64 cap = (u64)(H->pq_n[k] - s) * ppc;
+            const u32 first = H->pq_start[k] + s;
+            if (fl == FL_ARRAY) {
+                if (ring_fill(H->hq[k], cap, 1, first, ppc) != OURO_OK) return OURO_ERR_CUDA;
+                continue;
+            }
+            ouro_queue_dev& q = H->hq[k];
+            ouro_queue_dev& P = H->hq[K + 1 + k];
+            const u64 Sx = fl == FL_VA ? S_va : S_vl;
+            const u32 m = (u32)((cap + Sx - 1) / Sx);
+            const u32 seg0 = H->pq_start[k];
+            if (m) CK(cudaMemsetAsync(H->d_heap + ((u64)seg0 << g.chunk_shift), 0, (size_t)m << g.chunk_shift, st));
+            if (cap) {
+                k_fill_segments<<<std::min<u64>((cap + kBlock - 1) / kBlock, 148 * 64), kBlock, 0, st>>>(
+                    H->d_heap, g.chunk_shift, seg0, Sx, fl == FL_VA ? 0 : 2, cap, first, ppc, g.page_bits);
+                CK(cudaGetLastError());
+            }
+            q.count = (int64_t)cap;
+            q.tail = cap;
+            q.seg_live = q.seg_hwm = m;
+            if (fl == FL_VA) {
+                if (dir_init(q, m, seg0) != OURO_OK) return OURO_ERR_CUDA;
+            } else if (m) {
+                k_vl_headers<<<grid_for(m), kBlock, 0, st>>>(H->d_heap, g.chunk_shift, seg0, m);
+                CK(cudaGetLastError());
+                q.vl_head = ((u64)0 << 32) | seg0;
+                q.vl_tail = ((u64)(m - 1) << 32) | (seg0 + m - 1);
+            }
+            // private segment pool: reserve chunks not used by the prefill
+            std::vector<u64> ps(P.ring_mask + 1, 0);
+            for (u32 i = m; i < s; ++i) ps[i - m] = (1ull << 32) | (seg0 + i);
+            CK(cudaMemcpyAsync(P.slots, ps.data(), ps.size() * 8, cudaMemcpyHostToDevice, st));
+            CK(cudaStreamSynchronize(st));
+            P.count = (int64_t)(s - m);
+            P.tail = s - m;
+        }
+        if (ring_fill(H->hq[K], 0, 0, 0, 1) != OURO_OK) return OURO_ERR_CUDA;
+    } else {
+        if (ring_fill(H->hq[K], N, 0, 0, 1) != OURO_OK) return OURO_ERR_CUDA;
+        for (u32 k = 0; k < K; ++k) {
+            ouro_queue_dev& q = H->hq[k];
+            if (fl == FL_ARRAY) CK(cudaMemsetAsync(q.slots, 0, (q.ring_mask + 1) * 8, st));
+            else if (fl == FL_VA && dir_init(q, 0, 0) != OURO_OK) return OURO_ERR_CUDA;
+        }
+    }
+    CK(cudaMemcpyAsync(H->d_q, H->hq.data(), H->nq * sizeof(ouro_queue_dev), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    return OURO_OK;
+}
+
+void make_view(ouro_heap* H) {
+    const Geometry& g = H->g;
+    ouro_heap_view& v = H->view;
+    std::memset(&v, 0, sizeof(v));
+    v.base = H->d_heap;
+    v.meta = H->d_meta;
+    v.bitmap = H->d_bitmap;
+    v.assigned = H->d_assigned;
+    v.q = H->d_q;
+    v.ctr = H->d_ctr;
+    v.sticky = H->d_sticky;
+    v.heap_bytes = g.heap;
+    v.chunk_bytes = g.chunk;
+    v.S_va = g.chunk / 8;
+    v.S_vl = g.chunk / 8 - 2;
+    v.floor_F = H->floor_F;
+    v.spin_limit = 1ull << 22;
+    v.N = g.N;
+    v.K = g.K;
+    v.page_bits = g.page_bits;
+    v.chunk_bits = g.chunk_bits;
+    v.chunk_shift = g.chunk_shift;
+    v.min_shift = g.min_shift;
+    v.Wmax = g.Wmax;
+    v.gmask = g.gmask;
+    v.cmask = g.cmask;
+    v.kind = H->cfg.allocator_kind;
+    v.flavor = H->cfg.queue_flavor;
+    v.backoff = H->cfg.backoff;
+    v.max_retries = H->cfg.max_retries;
+    v.sleep_base_ns = H->cfg.sleep_base_ns;
+    v.sleep_cap_ns = H->cfg.sleep_cap_ns;
+}
+
+// Quiescent canonical digest + per-class recount (device passes, host finish).
+ouro_status compute_digest(ouro_heap* H, ouro_digest* out, DigestDev* hd_out, std::vector<ouro_queue_dev>* qs_out,
+                           cudaStream_t st) {
+    const Geometry& g = H->g;
+    const u32 N = g.N, K = g.K;
+    DigestDev* d = nullptr;
+    u32 *where = nullptr, *entries = nullptr;
+    CK(cudaMalloc(&d, sizeof(DigestDev)));
+    CK(cudaMalloc(&where, (size_t)N * 4));
+    CK(cudaMalloc(&entries, (size_t)N * 4));
+    CK(cudaMemsetAsync(d, 0, sizeof(DigestDev), st));
+    CK(cudaMemsetAsync(where, 0, (size_t)N * 4, st));
+    CK(cudaMemsetAsync(entries, 0, (size_t)N * 4, st));
+    std::vector<ouro_queue_dev> qs(H->nq);
+    CK(cudaMemcpyAsync(qs.data(), H->d_q, H->nq * sizeof(ouro_queue_dev), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    k_digest_headers<<<grid_for(N), kBlock, 0, st>>>(H->view, d, where);
+    CK(cudaGetLastError());
+    std::vector<u32> host_where_add(N, 0);
+    bool host_bad = false;
+    const u64 S_va = g.chunk / 8, S_vl = g.chunk / 8 - 2;
+    // segment table of a quiescent virtual queue (seq-indexed chunk ids)
+    auto segtab_of = [&](const ouro_queue_dev& q, std::vector<u32>& tab, u64& first) -> ouro_status {
+        tab.clear();
+        first = 0;
+        if (q.flavor == FL_ARRAY || q.tail == q.head) return OURO_OK;
+        const u64 Sx = q.flavor == FL_VA ? S_va : S_vl;
+        const u64 s0 = q.head / Sx, s1 = (q.tail - 1) / Sx;
+        first = s0;
+        tab.assign(s1 - s0 + 1, NONE);
+        if (q.flavor == FL_VA) {
+            std::vector<u64> dir(q.D);
+            CK(cudaMemcpy(dir.data(), q.dir, (size_t)q.D * 8, cudaMemcpyDeviceToHost));
+            for (u64 s = s0; s <= s1; ++s) {
+                const u64 e = dir[s % q.D];
+                if ((u32)(e >> 32) == (u32)s) tab[s - s0] = (u32)e;
+            }
+        } else {
+            u32 cur = (u32)q.vl_head;
+            u32 i = (u32)(q.vl_head >> 32);
+            u64 guard = 0;
+            while (cur != NONE && guard++ < (1ull << 26)) {
+                const u64 s = s0 + (u32)(i - (u32)s0);
+                if (s > s1) break;
+                if (s >= s0) tab[s - s0] = cur;
+                u64 nx;
+                CK(cudaMemcpy(&nx, H->d_heap + ((u64)cur << g.chunk_shift), 8, cudaMemcpyDeviceToHost));
+                cur = nx == NONE_LINK ? NONE : (u32)nx;
+                ++i;
+            }
+        }
+        return OURO_OK;
+    };
+    auto count_segments = [&](const ouro_queue_dev& q) -> ouro_status {
+        if (q.flavor == FL_VA) {
+            std::vector<u64> dir(q.D);
+            CK(cudaMemcpy(dir.data(), q.dir, (size_t)q.D * 8, cudaMemcpyDeviceToHost));
+            for (u32 i = 0; i < q.D; ++i)
+                if ((u32)dir[i] != NONE) { if ((u32)dir[i] < N) host_where_add[(u32)dir[i]]++; else host_bad = true; }
+        } else if (q.flavor == FL_VL) {
+            u32 cur = (u32)q.vl_head;
+            u64 guard = 0;
+            while (cur != NONE && guard++ < (1ull << 26)) {
+                if (cur < N) host_where_add[cur]++; else { host_bad = true; break; }
+                u64 nx;
+                CK(cudaMemcpy(&nx, H->d_heap + ((u64)cur << g.chunk_shift), 8, cudaMemcpyDeviceToHost));
+                cur = nx == NONE_LINK ? NONE : (u32)nx;
+            }
+        }
+        return OURO_OK;
+    };
+    auto run_queue = [&](u32 qi, int mode, u32 k) -> ouro_status {
+        const ouro_queue_dev& q = qs[qi];
+        const u64 n = q.tail - q.head;
+        if (n == 0) return OURO_OK;
+        std::vector<u32> tab;
+        u64 first;
+        if (segtab_of(q, tab, first) != OURO_OK) return OURO_ERR_CUDA;
+        u32* dtab = nullptr;
+        if (!tab.empty()) {
+            CK(cudaMalloc(&dtab, tab.size() * 4));
+            CK(cudaMemcpy(dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+        }
+        k_digest_queue<<<(unsigned)std::min<u64>((n + kBlock - 1) / kBlock, 148 * 32), kBlock, 0, st>>>(
+            H->view, H->d_q + qi, dtab, first, mode, k, d, where, entries);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        if (dtab) cudaFree(dtab);
+        return OURO_OK;
+    };
+    if (H->cfg.allocator_kind == OURO_KIND_CHUNK) {
+        if (run_queue(K, 0, 0) != OURO_OK) return OURO_ERR_CUDA;
+        for (u32 k = 0; k < K; ++k) {
+            if (count_segments(qs[k]) != OURO_OK) return OURO_ERR_CUDA;
+            if (run_queue(k, 2, k) != OURO_OK) return OURO_ERR_CUDA;
+        }
+    } else {
+        for (u32 k = 0; k < K; ++k) {
+            if (H->cfg.queue_flavor != FL_ARRAY) {
+                if (count_segments(qs[k]) != OURO_OK) return OURO_ERR_CUDA;
+                if (run_queue(K + 1 + k, 0, 0) != OURO_OK) return OURO_ERR_CUDA;
+            }
+            if (run_queue(k, 1, k) != OURO_OK) return OURO_ERR_CUDA;
+        }
+    }
+    DigestDev hd;
+    std::vector<u32> hw(N), he(N);
+    std::vector<u64> meta(N);
+    CK(cudaMemcpyAsync(&hd, d, sizeof(hd), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hw.data(), where, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(he.data(), entries, (size_t)N * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(meta.data(), H->d_meta, (size_t)N * 8, cudaMemcpyDeviceToHost, st));
+    u32 sticky[2];
+    CK(cudaMemcpyAsync(sticky, H->d_sticky, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFree(d);
+    cudaFree(where);
+    cudaFree(entries);
+    bool ok = hd.bad == 0 && !host_bad;
+    for (u32 c = 0; c < N; ++c) {
+        if (hw[c] + host_where_add[c] != 1) ok = false;
+        if (H->cfg.allocator_kind == OURO_KIND_CHUNK) {
+            const u32 s8 = (u32)(meta[c] >> 32) & 0xFF;
+            const bool has_free = s8 >= 1 && s8 <= K && (u32)meta[c] > 0;
+            if (he[c] != (has_free ? 1u : 0u)) ok = false;
+        }
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->num_chunks = N;
+    out->num_classes = K;
+    out->partition_ok = ok ? 1 : 0;
+    out->sticky_mask = sticky[1];
+    out->live_pages = hd.live_pages;
+    out->unassigned_chunks = N - hd.assigned_total;
+    out->header_hash = hd.header_hash;
+    out->queue_hash = hd.queue_hash;
+    for (u32 k = 0; k < K; ++k) {
+        out->class_chunks[k] = hd.class_chunks[k];
+        out->class_queued_live[k] = hd.class_queued_live[k];
+        out->class_live_pages[k] = hd.class_live_pages[k];
+    }
+    if (hd_out) *hd_out = hd;
+    if (qs_out) *qs_out = qs;
+    return OURO_OK;
+}
+
+}  // namespace
+
+// =================================================================== C ABI ====
+extern "C" {
+
+ouro_status ouro_heap_create(const ouro_config* cfg, int device, ouro_heap** out) {
+    if (!cfg || !out) return OURO_ERR_USAGE;
+    ouro_host::Geometry g;
+    if (ouro_host::geometry(cfg, &g) != OURO_OK) return OURO_ERR_CONFIG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) return OURO_ERR_CUDA;
+    CK(cudaSetDevice(device));
+    auto* H = new ouro_heap();
+    H->cfg = *cfg;
+    H->g = g;
+    H->device = device;
+    auto fail = [&](ouro_status s) { ouro_heap_destroy(H); return s; };
+    H->d_heap = static_cast<uint8_t*>(dalloc(H, g.heap));
+    H->d_meta = static_cast<u64*>(dalloc(H, (size_t)g.N * 8));
+    H->d_bitmap = static_cast<u64*>(dalloc(H, (size_t)g.N * g.Wmax * 8));
+    H->d_assigned = static_cast<u32*>(dalloc(H, (size_t)g.K * 4));
+    H->d_ctr = static_cast<u64*>(dalloc(H, (size_t)(2 * g.K + OURO_CTR_N) * 8));
+    H->d_sticky = static_cast<u32*>(dalloc(H, 8));
+    if (!H->d_heap || !H->d_meta || !H->d_bitmap || !H->d_assigned || !H->d_ctr || !H->d_sticky) return fail(OURO_ERR_CUDA);
+    if (plan(H) != OURO_OK) return fail(OURO_ERR_CUDA);
+    H->d_q = static_cast<ouro_queue_dev*>(dalloc(H, H->nq * sizeof(ouro_queue_dev)));
+    if (!H->d_q) return fail(OURO_ERR_CUDA);
+    make_view(H);
+    const ouro_status s = fill(H, 0);
+    if (s != OURO_OK) return fail(s);
+    *out = H;
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_destroy(ouro_heap* H) {
+    if (!H) return OURO_ERR_USAGE;
+    cudaSetDevice(H->device);
+    for (void* p : H->owned) cudaFree(p);
+    if (H->d_touched) cudaFree(H->d_touched);
+    delete H;
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_reset(ouro_heap* H, void* stream) {
+    if (!H) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    CK(cudaStreamSynchronize(S(stream)));
+    return fill(H, S(stream));
+}
+
+size_t ouro_heap_view_size(void) { return sizeof(ouro_heap_view); }
+
+ouro_status ouro_heap_get_view(const ouro_heap* H, void* out, size_t size) {
+    if (!H || !out || size < sizeof(ouro_heap_view)) return OURO_ERR_USAGE;
+    std::memcpy(out, &H->view, sizeof(ouro_heap_view));
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_config(const ouro_heap* H, ouro_config* cfg, ouro_geometry* geo) {
+    if (!H) return OURO_ERR_USAGE;
+    if (cfg) *cfg = H->cfg;
+    if (geo) return ouro_config_geometry(&H->cfg, geo);
+    return OURO_OK;
+}
+
+uint64_t ouro_heap_base(const ouro_heap* H) { return H ? (uint64_t)(uintptr_t)H->d_heap : 0; }
+
+ouro_status ouro_page_region(ouro_heap* H, uint32_t h, uint64_t* offset, uint64_t* len) {
+    if (!H) return OURO_ERR_USAGE;
+    const Geometry& g = H->g;
+    const u64 c = (u64)h >> g.page_bits;
+    const u32 p = h & ((1u << g.page_bits) - 1u);
+    if (c >= g.N) return OURO_ERR_RANGE;
+    u64 m;
+    CK(cudaMemcpy(&m, H->d_meta + c, 8, cudaMemcpyDeviceToHost));
+    const u32 st = (u32)(m >> 32) & 0xFF;
+    if (st == 0 || st == 0xFF || st > g.K) return OURO_ERR_INVALID_HANDLE;
+    const u32 k = st - 1;
+    if (p >= g.ppc(k)) return OURO_ERR_INVALID_HANDLE;
+    *offset = (c << g.chunk_shift) + ((u64)p << (g.min_shift + k));
+    *len = g.page_bytes(k);
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_last_error(ouro_heap* H, uint32_t* first, uint32_t* mask, int clear) {
+    if (!H) return OURO_ERR_USAGE;
+    u32 s[2];
+    CK(cudaMemcpy(s, H->d_sticky, 8, cudaMemcpyDeviceToHost));
+    if (first) *first = s[0];
+    if (mask) *mask = s[1];
+    if (clear) CK(cudaMemset(H->d_sticky, 0, 8));
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_digest(ouro_heap* H, ouro_digest* out, void* stream) {
+    if (!H || !out) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    CK(cudaStreamSynchronize(S(stream)));
+    return compute_digest(H, out, nullptr, nullptr, S(stream));
+}
+
+ouro_status ouro_heap_stats(ouro_heap* H, ouro_stats* out, void* stream) {
+    if (!H || !out) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    CK(cudaStreamSynchronize(S(stream)));
+    ouro_digest dg;
+    DigestDev hd;
+    std::vector<ouro_queue_dev> qs;
+    const ouro_status s = compute_digest(H, &dg, &hd, &qs, S(stream));
+    if (s != OURO_OK) return s;
+    const Geometry& g = H->g;
+    std::vector<u64> ctr(2 * g.K + OURO_CTR_N);
+    u32 sticky[2];
+    CK(cudaMemcpy(ctr.data(), H->d_ctr, ctr.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sticky, H->d_sticky, 8, cudaMemcpyDeviceToHost));
+    std::memset(out, 0, sizeof(*out));
+    out->num_classes = g.K;
+    out->num_chunks = g.N;
+    out->sticky_first = sticky[0];
+    out->sticky_mask = sticky[1];
+    const u64* c = ctr.data() + 2 * g.K;
+    out->stale_drops = c[OURO_CTR_STALE];
+    out->double_frees = c[OURO_CTR_DOUBLE_FREE];
+    out->invalid_frees = c[OURO_CTR_INVALID_FREE];
+    out->bad_sizes = c[OURO_CTR_BAD_SIZE];
+    out->timeouts = c[OURO_CTR_TIMEOUT];
+    out->corruptions = c[OURO_CTR_CORRUPTION];
+    if (H->cfg.allocator_kind == OURO_KIND_CHUNK) out->pool_len = (u64)qs[g.K].count;
+    for (u32 k = 0; k < g.K; ++k) {
+        ouro_class_stats& cs = out->cls[k];
+        cs.page_bytes = g.page_bytes(k);
+        cs.pages_per_chunk = g.ppc(k);
+        cs.chunks = hd.class_chunks[k];
+        cs.live_pages = hd.class_live_pages[k];
+        cs.queue_len = (u64)qs[k].count;
+        cs.queued_live = hd.class_queued_live[k];
+        cs.seg_live = qs[k].seg_live;
+        cs.seg_hwm = qs[k].seg_hwm;
+        cs.retries = ctr[k];
+        cs.ooms = ctr[g.K + k];
+    }
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_alloc(ouro_heap* H, uint64_t n, uint64_t uniform_bytes, const uint32_t* d_sizes, void** d_out,
+                              void* stream) {
+    if (!H || !d_out) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    OURO_VSWITCH(H, launch_alloc, H, n, uniform_bytes, d_sizes, d_out, S(stream));
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_free(ouro_heap* H, uint64_t n, void* const* d_ptrs, void* stream) {
+    if (!H || !d_ptrs) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    OURO_VSWITCH(H, launch_free, H, n, d_ptrs, S(stream));
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_write(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t seed, uint32_t it, void* stream) {
+    if (!H || !d_ptrs) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    k_pattern<false><<<grid_for(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, nullptr);
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_verify(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t seed, uint32_t it,
+                               uint64_t* d_result, void* stream) {
+    if (!H || !d_ptrs || !d_result) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    k_pattern<true><<<grid_for(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, reinterpret_cast<u64*>(d_result));
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_count(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t* d_count, void* stream) {
+    if (!H || !d_ptrs || !d_count) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    k_count<<<grid_for(n), kBlock, 0, S(stream)>>>(n, d_ptrs, reinterpret_cast<u64*>(d_count));
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_audit(ouro_heap* H, uint64_t n, void* const* d_ptrs, ouro_audit_result* out, void* stream) {
+    if (!H || !d_ptrs || !out) return OURO_ERR_USAGE;
+    std::memset(out, 0, sizeof(*out));
+    if (n == 0) return OURO_OK;
+    cudaStream_t st = S(stream);
+    u64 *offs, *lens, *offs2, *lens2, *res;
+    unsigned long long* idx;
+    CK(cudaMalloc(&offs, n * 8));
+    CK(cudaMalloc(&lens, n * 8));
+    CK(cudaMalloc(&offs2, n * 8));
+    CK(cudaMalloc(&lens2, n * 8));
+    CK(cudaMalloc(&res, 8 * 8));
+    CK(cudaMalloc(&idx, 8));
+    CK(cudaMemsetAsync(res, 0, 64, st));
+    CK(cudaMemsetAsync(idx, 0, 8, st));
+    k_audit_collect<<<grid_for(n), kBlock, 0, st>>>(H->view, n, d_ptrs, offs, lens, res, idx);
+    CK(cudaGetLastError());
+    u64 m = 0;
+    CK(cudaMemcpyAsync(&m, idx, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (m > 1) {
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st);
+        void* tmp;
+        CK(cudaMalloc(&tmp, tb));
+        cub::DeviceRadixSort::SortPairs(tmp, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st);
+        k_audit_neighbours<<<grid_for(m), kBlock, 0, st>>>(m, offs2, lens2, res);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        cudaFree(tmp);
+    }
+    u64 r[8];
+    CK(cudaMemcpyAsync(r, res, 64, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out->live = r[0];
+    out->out_of_heap = r[1];
+    out->misaligned = r[2];
+    out->overlaps = r[3];
+    out->not_marked = r[4];
+    out->bytes = r[5];
+    cudaFree(offs); cudaFree(lens); cudaFree(offs2); cudaFree(lens2); cudaFree(res); cudaFree(idx);
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_churn(ouro_heap* H, uint64_t n, uint32_t round_begin, uint32_t rounds, uint64_t seed,
+                              void** d_slots, uint64_t* d_result, void* stream) {
+    if (!H || !d_slots || !d_result) return OURO_ERR_USAGE;
+    if (!H->d_touched) {
+        const size_t b = H->g.heap / H->g.minp / 8 + 8;
+        CK(cudaMalloc(&H->d_touched, b));
+        CK(cudaMemset(H->d_touched, 0, b));
+    }
+    for (uint32_t r = round_begin; r < round_begin + rounds; ++r) {
+        OURO_VSWITCH(H, launch_churn, H, n, r, seed, d_slots, reinterpret_cast<u64*>(d_result), S(stream));
+    }
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_run_script(ouro_heap* H, const ouro_script_step* steps, uint32_t nsteps, uint64_t* out_offset,
+                            int32_t* out_status) {
+    if (!H || !steps || !out_offset || !out_status) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    ouro_script_step* ds;
+    u64* doff;
+    int* dst;
+    CK(cudaMalloc(&ds, (size_t)nsteps * sizeof(ouro_script_step) + 1));
+    CK(cudaMalloc(&doff, (size_t)nsteps * 32 * 8 + 8));
+    CK(cudaMalloc(&dst, (size_t)nsteps * 32 * 4 + 4));
+    CK(cudaMemcpy(ds, steps, (size_t)nsteps * sizeof(ouro_script_step), cudaMemcpyHostToDevice));
+    OURO_VSWITCH(H, launch_script, H, ds, nsteps, doff, dst);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out_offset, doff, (size_t)nsteps * 32 * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out_status, dst, (size_t)nsteps * 32 * 4, cudaMemcpyDeviceToHost));
+    cudaFree(ds); cudaFree(doff); cudaFree(dst);
+    return OURO_OK;
+}
+
+// run_trial: host buffers in, host results out.
+ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial_result* out) {
+    if (!H || !tc || !out) return OURO_ERR_USAGE;
+    if (tc->iterations < 2 || tc->iterations > 64 || tc->num_allocations == 0) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    std::memset(out, 0, sizeof(*out));
+    const u64 n = tc->num_allocations;
+    cudaStream_t st;
+    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    void** ptrs;
+    u32* dsz = nullptr;
+    u64* dres;
+    CK(cudaMalloc(&ptrs, n * sizeof(void*)));
+    if (tc->sizes) CK(cudaMalloc(&dsz, n * 4));
+    CK(cudaMalloc(&dres, 4 * 8));
+    cudaEvent_t ev[6];
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    bool verified = true;
+    for (u32 it = 0; it < tc->iterations; ++it) {
+        const u64 init[4] = {0, ~0ull, 0, 0};
+        CK(cudaMemcpyAsync(dres, init, 32, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(ev[0], st));
+        if (tc->sizes) CK(cudaMemcpyAsync(dsz, tc->sizes, n * 4, cudaMemcpyHostToDevice, st));
+        if (ouro_launch_alloc(H, n, tc->allocation_bytes, dsz, ptrs, st) != OURO_OK) return OURO_ERR_CUDA;
+        CK(cudaEventRecord(ev[1], st));
+        ouro_launch_write(H, n, ptrs, tc->seed, it, st);
+        CK(cudaEventRecord(ev[2], st));
+        ouro_launch_verify(H, n, ptrs, tc->seed, it, reinterpret_cast<uint64_t*>(dres), st);
+        ouro_launch_count(H, n, ptrs, reinterpret_cast<uint64_t*>(dres + 2), st);
+        CK(cudaEventRecord(ev[3], st));
+        ouro_launch_free(H, n, ptrs, st);
+        CK(cudaEventRecord(ev[4], st));
+        u64 r[4];
+        CK(cudaMemcpyAsync(r, dres, 32, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        float a, w, vv, f;
+        cudaEventElapsedTime(&a, ev[0], ev[1]);
+        cudaEventElapsedTime(&w, ev[1], ev[2]);
+        cudaEventElapsedTime(&vv, ev[2], ev[3]);
+        cudaEventElapsedTime(&f, ev[3], ev[4]);
+        out->alloc_ms[it] = a;
+        out->write_ms[it] = w;
+        out->verify_ms[it] = vv;
+        out->free_ms[it] = f;
+        out->ok_allocs += r[2];
+        out->failed_allocs += n - r[2];
+        if (r[0] != 0) verified = false;
+    }
+    out->iterations = tc->iterations;
+    out->verified = verified ? 1 : 0;
+    ouro_trial_means(out->alloc_ms, tc->iterations, &out->mean_all_ms, &out->mean_subsequent_ms);
+    double fa;
+    ouro_trial_means(out->free_ms, tc->iterations, &fa, &out->mean_subsequent_free_ms);
+    out->h2d_bytes = tc->sizes ? n * 4 : 0;
+    out->d2h_bytes = 32;
+    for (auto& e : ev) cudaEventDestroy(e);
+    cudaFree(ptrs);
+    if (dsz) cudaFree(dsz);
+    cudaFree(dres);
+    cudaStreamDestroy(st);
+    return OURO_OK;
+}
+
+ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
+    if (!ops_per_s) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(device));
+    const u64 words = 1ull << 22;  // 32 MiB of u64 / 16 MiB of u32 counters: L2-resident (atomics resolve in L2)
+    void* buf;
+    CK(cudaMalloc(&buf, words * 8));
+    CK(cudaMemset(buf, 0, words * 8));
+    const unsigned blocks = 148 * 8, threads = 256;
+    const u32 iters = mode >= 2 ? 64 : 64;
+    cudaEvent_t a, b;
+    CK(cudaEventCreate(&a));
+    CK(cudaEventCreate(&b));
+    auto run = [&]() {
+        switch (mode) {
+        case 0: k_atom_distinct32<<<blocks, threads>>>((u32*)buf, words * 2, iters); break;
+        case 1: k_atom_distinct_cas64<<<blocks, threads>>>((u64*)buf, words, iters); break;
+        case 2: k_atom_same_warp<<<blocks, threads>>>((u64*)buf, iters); break;
+        default: k_atom_same_lane<<<blocks, threads>>>((u64*)buf, iters / 16); break;
+        }
+    };
+    run();
+    CK(cudaDeviceSynchronize());
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        CK(cudaEventRecord(a));
+        run();
+        CK(cudaEventRecord(b));
+        CK(cudaEventSynchronize(b));
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        best = std::min(best, ms);
+    }
+    CK(cudaGetLastError());
+    double ops = (double)blocks * threads * iters;
+    if (mode == 2) ops /= 32.0;
+    if (mode == 3) ops = (double)blocks * threads * (iters / 16);
+    *ops_per_s = ops / (best * 1e-3);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    return OURO_OK;
+}
+
+const char* ouro_build_info(void) {
+    return "libouro_b200 sm_100a (" __DATE__ " " __TIME__ ")";
+}
+
+}  // extern "C"
