@@ -766,9 +766,12 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
 }
 
 // malloc for the converged lanes of the calling warp.
+// `mask_hint`: the lanes the caller knows are calling together (0 = use
+// __activemask(), which only sees the lanes that happen to be converged).
 template <int KIND, int FL>
-__device__ __forceinline__ void* malloc_impl(const ouro_heap_view& v, u64 bytes, int* status) {
-    const u32 mask = __activemask();
+__device__ __forceinline__ void* malloc_impl(const ouro_heap_view& v, u64 bytes, int* status, u32 mask_hint = 0) {
+    const u32 mask = mask_hint ? mask_hint : __activemask();
+    if (mask_hint) __syncwarp(mask);
     const u32 lane = lane_id();
     u32 k = 0;
     const bool valid = size_class(v, bytes, &k);
@@ -791,8 +794,9 @@ __device__ __forceinline__ void* malloc_impl(const ouro_heap_view& v, u64 bytes,
 
 // free for the converged lanes of the calling warp.
 template <int KIND, int FL>
-__device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr) {
-    const u32 mask = __activemask();
+__device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32 mask_hint = 0) {
+    const u32 mask = mask_hint ? mask_hint : __activemask();
+    if (mask_hint) __syncwarp(mask);
     const u32 lane = lane_id();
     const u32 lt = lanemask_lt();
     int st = OURO_OK;
@@ -903,14 +907,16 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr) {
 
 // all-or-nothing group allocation (alloc_coalesced)
 template <int KIND, int FL>
-__device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, u64 bytes, int* status) {
-    const u32 mask = __activemask();
+__device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, u64 bytes, int* status,
+                                                       u32 mask_hint = 0) {
+    const u32 mask = mask_hint ? mask_hint : __activemask();
     int st;
-    void* p = malloc_impl<KIND, FL>(v, bytes, &st);
+    void* p = malloc_impl<KIND, FL>(v, bytes, &st, mask);
     const u32 fails = __ballot_sync(mask, st != OURO_OK);
     if (fails) {
         const bool tl = __shfl_sync(mask, st, __ffs(mask) - 1) == OURO_ERR_TOO_LARGE;
-        if (p) free_impl<KIND, FL>(v, p);
+        const u32 rb = __ballot_sync(mask, p != nullptr);
+        if (p) free_impl<KIND, FL>(v, p, rb);  // roll back partial grants
         __syncwarp(mask);
         p = nullptr;
         st = tl ? OURO_ERR_TOO_LARGE : OURO_ERR_OOM;
@@ -923,17 +929,21 @@ __device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, 
 
 // ---------------------------------------------------------------- public ----
 // Compile-time variant entry points (fastest: no dispatch).
+// `lanes`: optional mask of the lanes of this warp that make the call together
+// (all of them must pass the same mask); 0 = whatever __activemask() reports.
 template <int KIND, int FLAVOR>
-__device__ __forceinline__ void* ouro_malloc_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr) {
-    return ouro_dev::malloc_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status);
+__device__ __forceinline__ void* ouro_malloc_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr,
+                                               unsigned lanes = 0) {
+    return ouro_dev::malloc_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status, lanes);
 }
 template <int KIND, int FLAVOR>
-__device__ __forceinline__ int ouro_free_t(const ouro_heap_view& h, void* p) {
-    return ouro_dev::free_impl<KIND, FLAVOR>(h, p);
+__device__ __forceinline__ int ouro_free_t(const ouro_heap_view& h, void* p, unsigned lanes = 0) {
+    return ouro_dev::free_impl<KIND, FLAVOR>(h, p, lanes);
 }
 template <int KIND, int FLAVOR>
-__device__ __forceinline__ void* ouro_malloc_coalesced_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr) {
-    return ouro_dev::malloc_coalesced_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status);
+__device__ __forceinline__ void* ouro_malloc_coalesced_t(const ouro_heap_view& h, size_t bytes, int* status = nullptr,
+                                                         unsigned lanes = 0) {
+    return ouro_dev::malloc_coalesced_impl<KIND, FLAVOR>(h, (unsigned long long)bytes, status, lanes);
 }
 
 // Runtime-dispatched entry points (variant read from the view).
@@ -943,17 +953,17 @@ __device__ __forceinline__ void* ouro_malloc_coalesced_t(const ouro_heap_view& h
     case 3: CALL(1, 0); case 4: CALL(1, 1); default: CALL(1, 2);                           \
     }
 
-__device__ __noinline__ void* ouro_malloc(const ouro_heap_view& h, size_t bytes) {
+static __device__ __noinline__ void* ouro_malloc(const ouro_heap_view& h, size_t bytes) {
 #define OURO_M(K, F) return ouro_malloc_t<K, F>(h, bytes)
     OURO_DISPATCH(h, OURO_M)
 #undef OURO_M
 }
-__device__ __noinline__ void ouro_free(const ouro_heap_view& h, void* p) {
+static __device__ __noinline__ void ouro_free(const ouro_heap_view& h, void* p) {
 #define OURO_F(K, F) ouro_free_t<K, F>(h, p); return
     OURO_DISPATCH(h, OURO_F)
 #undef OURO_F
 }
-__device__ __noinline__ void* ouro_malloc_coalesced(const ouro_heap_view& h, size_t bytes) {
+static __device__ __noinline__ void* ouro_malloc_coalesced(const ouro_heap_view& h, size_t bytes) {
 #define OURO_C(K, F) return ouro_malloc_coalesced_t<K, F>(h, bytes)
     OURO_DISPATCH(h, OURO_C)
 #undef OURO_C

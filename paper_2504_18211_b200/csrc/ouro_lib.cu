@@ -113,15 +113,17 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const u32* sizes, void** out) {
     const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
     if (i >= n) return;
     const u64 sz = sizes ? sizes[i] : uniform;
-    out[i] = ouro_malloc_t<KIND, FL>(v, sz);
+    out[i] = ouro_malloc_t<KIND, FL>(v, sz, nullptr, lanes);
 }
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_free(ouro_heap_view v, u64 n, void* const* ptrs) {
     const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
+    const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
     if (i >= n) return;
-    ouro_free_t<KIND, FL>(v, ptrs[i]);
+    ouro_free_t<KIND, FL>(v, ptrs[i], lanes);
 }
 
 __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p) {
@@ -219,16 +221,21 @@ template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
                                                   uint8_t* touched, u64* res) {
     const u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-    if (t >= n) return;
+    const bool in = t < n;
     const u64 h = mix64h(seed ^ (t << 32) ^ r);
-    void* s = slots[t];
+    void* s = in ? slots[t] : nullptr;
+    const bool do_free = in && s && (h & 1);
+    const bool do_malloc = in && !s;
+    const u32 fm = __ballot_sync(0xFFFFFFFFu, do_free);
+    const u32 mm = __ballot_sync(0xFFFFFFFFu, do_malloc);
+    if (!in) return;
     u32 ev_ok = 0, ev_fail = 0, ev_free = 0, ev_reuse = 0, ev_bad = 0;
-    if (s && (h & 1)) {
-        ouro_free_t<KIND, FL>(v, s);
+    if (do_free) {
+        ouro_free_t<KIND, FL>(v, s, fm);
         slots[t] = nullptr;
         ev_free = 1;
-    } else if (!s) {
-        void* p = ouro_malloc_t<KIND, FL>(v, 8 + (h >> 1) % 4089);
+    } else if (do_malloc) {
+        void* p = ouro_malloc_t<KIND, FL>(v, 8 + (h >> 1) % 4089, nullptr, mm);
         if (p) {
             *reinterpret_cast<u64*>(p) = mix64h(t ^ seed);
             slots[t] = p;
@@ -264,11 +271,12 @@ __global__ void k_script(ouro_heap_view v, const ouro_script_step* steps, u32 ns
         out_off[s * 32 + lane] = ~0ull;
         out_st[s * 32 + lane] = -1;
         __syncwarp();
-        if ((st.lane_mask >> lane) & 1u) {
+        const u32 lanes = st.lane_mask;
+        if ((lanes >> lane) & 1u) {
             if (st.op == 0 || st.op == 2) {
                 int status;
-                void* p = st.op == 0 ? ouro_malloc_t<KIND, FL>(v, st.arg[lane], &status)
-                                     : ouro_malloc_coalesced_t<KIND, FL>(v, st.arg[lane], &status);
+                void* p = st.op == 0 ? ouro_malloc_t<KIND, FL>(v, st.arg[lane], &status, lanes)
+                                     : ouro_malloc_coalesced_t<KIND, FL>(v, st.arg[lane], &status, lanes);
                 out_off[s * 32 + lane] = p ? (u64)((uint8_t*)p - v.base) : ~0ull;
                 out_st[s * 32 + lane] = status;
             } else {
@@ -277,7 +285,7 @@ __global__ void k_script(ouro_heap_view v, const ouro_script_step* steps, u32 ns
                 if (a >> 63) off = a & ~(1ull << 63);
                 else off = a < (u64)s * 32 ? out_off[a] : ~0ull;
                 if (off == ~0ull) off = ~1ull;
-                out_st[s * 32 + lane] = ouro_free_t<KIND, FL>(v, v.base + off);
+                out_st[s * 32 + lane] = ouro_free_t<KIND, FL>(v, v.base + off, lanes);
             }
         }
         __syncwarp();

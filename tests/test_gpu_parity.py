@@ -32,10 +32,15 @@ def _script_parity(c, steps):
     goff, gst = h.run_script(steps)
     oh = OHeap(c)
     ooff, ost = oh.run_script(steps)
-    for i, (a, b) in enumerate(zip(gst, ost)):
-        assert a == b, f"status mismatch at step {i // 32} lane {i % 32}: gpu {a} oracle {b}"
-    for i, (a, b) in enumerate(zip(goff, ooff)):
-        assert a == b, f"offset mismatch at step {i // 32} lane {i % 32}: gpu {a} oracle {b}"
+    for i in range(len(gst)):
+        if gst[i] != ost[i] or goff[i] != ooff[i]:
+            s = i // 32
+            op, mask, args = steps[s]
+            lanes = [j for j in range(32) if mask >> j & 1]
+            detail = [(j, args[j], gst[s * 32 + j], ost[s * 32 + j], goff[s * 32 + j], ooff[s * 32 + j])
+                      for j in lanes]
+            raise AssertionError(f"first mismatch at step {s} lane {i % 32} op {op}: "
+                                 f"(lane, arg, gpu st, oracle st, gpu off, oracle off) = {detail}")
     gd, od = h.digest().as_dict(), oh.digest().as_dict()
     assert gd == od
     gs, os_ = h.stats(), oh.stats()
@@ -89,40 +94,48 @@ def test_coalesced_script_parity(cuda, variant):
     _script_parity(cfg(kind, flavor, 1 << 20, retries=2), steps)
 
 
-def _oracle_digest_for(c, sizes):
-    """The oracle's canonical digest after allocating `sizes` (warps of 32 lanes
-    in slot order) and freeing everything."""
+def _oracle_run(c, sizes):
+    """The oracle on the same demand (warps of 32 lanes in slot order): number
+    of successful allocations, and the canonical digest after freeing them."""
     oh = OHeap(c)
     offs = []
+    ok = 0
     for i in range(0, len(sizes), 32):
         o, s = oh.alloc(sizes[i:i + 32])
-        assert all(x == 0 for x in s)
-        offs += o
+        offs += [x for x, st in zip(o, s) if st == 0]
+        ok += sum(1 for st in s if st == 0)
     for i in range(0, len(offs), 32):
         assert all(x == 0 for x in oh.free(offs[i:i + 32]))
     d = oh.digest().as_dict()
     oh.close()
-    return d
+    return ok, d
+
+
+def _heap_bytes(kind):
+    # page kind: exact static partition (capacity identical on GPU and oracle);
+    # chunk kind: room for warp herding (each warp's group may open a chunk)
+    return (64 << 20) if kind == 0 else (256 << 20)
 
 
 @pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
 @pytest.mark.parametrize("size", [16, 1000, 8192])
 def test_concurrent_phased(cuda, variant, size):
-    """BASELINE configs[0] shape: 64 MiB heap, 65 536 threads, alloc/write/verify/free."""
+    """BASELINE configs[0] shape: 65 536 threads, alloc/audit/write/verify/free x3."""
     torch = cuda
     kind, flavor = variant
-    c = cfg(kind, flavor, 64 << 20, retries=64)
-    n = 65536 if size <= 1000 else 4096
+    c = cfg(kind, flavor, _heap_bytes(kind), retries=64)
+    n = 65536 if size <= 1000 else 8192
+    want_ok, want_digest = _oracle_run(c, [size] * n)
     h = _heap(c)
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
-    res = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
     for it in range(3):
+        res = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
         h.launch_alloc(n, ptrs, size=size)
         h.launch_count(n, ptrs, res[2:3])
         torch.cuda.synchronize()
-        assert int(res[2]) == n * (it + 1), "allocation failed under capacity"
+        assert int(res[2]) == want_ok, "success count differs from the oracle"
         a = h.audit(n, ptrs)
-        assert (a.live, a.out_of_heap, a.misaligned, a.overlaps, a.not_marked) == (n, 0, 0, 0, 0)
+        assert (a.live, a.out_of_heap, a.misaligned, a.overlaps, a.not_marked) == (want_ok, 0, 0, 0, 0)
         h.launch_write(n, ptrs, 1234, it)
         h.launch_verify(n, ptrs, 1234, it, res)
         torch.cuda.synchronize()
@@ -131,8 +144,7 @@ def test_concurrent_phased(cuda, variant, size):
         torch.cuda.synchronize()
     first, mask = h.last_error()
     assert first == 0, f"sticky device error {first} mask {mask:#x}"
-    gd = h.digest().as_dict()
-    assert gd == _oracle_digest_for(c, [size] * n)
+    assert h.digest().as_dict() == want_digest
     h.close()
 
 
@@ -140,10 +152,11 @@ def test_concurrent_phased(cuda, variant, size):
 def test_concurrent_mixed_sizes(cuda, variant):
     torch = cuda
     kind, flavor = variant
-    c = cfg(kind, flavor, 64 << 20, retries=64)
+    c = cfg(kind, flavor, _heap_bytes(kind), retries=64)
     n = 65536
     g = torch.Generator().manual_seed(5)
     sizes = torch.randint(1, 513, (n,), generator=g, dtype=torch.int32)
+    want_ok, want_digest = _oracle_run(c, sizes.tolist())
     h = _heap(c)
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
     dsz = sizes.cuda()
@@ -151,14 +164,14 @@ def test_concurrent_mixed_sizes(cuda, variant):
     h.launch_alloc(n, ptrs, sizes=dsz)
     h.launch_count(n, ptrs, res[2:3])
     torch.cuda.synchronize()
-    assert int(res[2]) == n
+    assert int(res[2]) == want_ok
     a = h.audit(n, ptrs)
-    assert (a.live, a.out_of_heap, a.misaligned, a.overlaps, a.not_marked) == (n, 0, 0, 0, 0)
+    assert (a.live, a.out_of_heap, a.misaligned, a.overlaps, a.not_marked) == (want_ok, 0, 0, 0, 0)
     h.launch_write(n, ptrs, 9, 0)
     h.launch_verify(n, ptrs, 9, 0, res)
     h.launch_free(n, ptrs)
     torch.cuda.synchronize()
     assert int(res[0]) == 0
     assert h.last_error()[0] == 0
-    assert h.digest().as_dict() == _oracle_digest_for(c, sizes.tolist())
+    assert h.digest().as_dict() == want_digest
     h.close()
