@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py -- malloc+free throughput of the B200 device allocator.
+
+Metric (BASELINE.json): malloc+free ops/sec vs size (16 B-8 KiB, 1M threads);
+% of L2-atomic roofline.
+
+Default workload = BASELINE configs[1]: page allocator, standard (Array)
+queues, 1 GiB heap, 2^20 device threads, size sweep 4 B ... 8 KiB (powers of
+two plus the paper's 1000 B).  One *step* = one pass over the sweep: for each
+size, 2^20 threads malloc (timed kernel), write + verify the pattern (checked,
+not in the metric), free (timed kernel).  L2 is flushed (256 MiB write) before
+every timed kernel.  value = successful malloc+free pairs / (sum of alloc +
+free kernel time), device-timed with CUDA events, max over ranks for N>1
+(weak scaling: every GPU owns an independent heap and the same per-GPU work).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config pq1g|cq64m|va8g|...]
+  python bench.py --impl reference ...   # the reference CPU allocator (oracle port)
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+SWEEP = [4, 8, 16, 32, 64, 128, 256, 512, 1000, 1024, 2048, 4096, 8192]
+CONFIGS = {
+    # name: (description, kind, flavor, heap, threads, sizes)
+    "cq64m": ("configs[0]: chunk allocator, Array queues, 64 MiB heap, 65536 threads x malloc(16)",
+              1, 0, 64 << 20, 65536, [16]),
+    "pq1g": ("configs[1]: page allocator (PQ), Array queues, 1 GiB heap, 1M threads, size sweep 4 B-8 KiB",
+             0, 0, 1 << 30, 1 << 20, SWEEP),
+    "vapq8g": ("configs[2]: VAPQ, 8 GiB heap, 1M threads, 16 B-8 KiB", 0, 1, 8 << 30, 1 << 20, SWEEP[2:]),
+    "vacq8g": ("configs[2]: VACQ, 8 GiB heap, 1M threads, 16 B-8 KiB", 1, 1, 8 << 30, 1 << 20, SWEEP[2:]),
+    "vlpq8g": ("configs[2]: VLPQ, 8 GiB heap, 1M threads, 16 B-8 KiB", 0, 2, 8 << 30, 1 << 20, SWEEP[2:]),
+    "vlcq8g": ("configs[2]: VLCQ, 8 GiB heap, 1M threads, 16 B-8 KiB", 1, 2, 8 << 30, 1 << 20, SWEEP[2:]),
+    "cq1g": ("chunk allocator (CQ), Array queues, 1 GiB heap, 1M threads, 16 B-8 KiB", 1, 0, 1 << 30, 1 << 20, SWEEP[2:]),
+    "pq16g4m": ("configs[4] per GPU: PQ, 16 GiB heap, 4M threads, 16 B-1 KiB", 0, 0, 16 << 30, 1 << 22,
+                [16, 32, 64, 128, 256, 512, 1000, 1024]),
+}
+HEADLINE_RANGE = (16, 1024)  # BASELINE target band
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="pq1g", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-threads", type=int, default=0)
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------- clocks ----
+REASONS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+    0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+    0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    """nvidia-smi sampled every 100 ms during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,utilization.gpu",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons, busy = [], 0, set(), []
+        for ln in self.lines:
+            try:
+                a, b, r, u = [x.strip() for x in ln.split(",")]
+                sm.append(float(a))
+                mx = max(mx, float(b))
+                code = int(r, 16)
+                for bit, name in REASONS.items():
+                    if code & bit:
+                        reasons.add(name)
+                busy.append(float(u))
+            except Exception:
+                continue
+        loaded = [s for s, u in zip(sm, busy) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons - {"gpu_idle"}), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference ----
+def run_reference(args, cfgname):
+    """The reference CPU allocator: the SPEC-faithful oracle restatement
+    (oracle/ouro_oracle.cpp; the reference tree has no runnable allocator),
+    on all host threads, one bounded sample of the same workload per step."""
+    from oracle_lib import OHeap, TrialOut, oracle
+    from paper_2504_18211_b200._abi import Config
+    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    threads = args.ref_threads or os.cpu_count() or 1
+    sample = min(n, 1 << 17)
+    cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
+    L = oracle()
+    oh = OHeap(cfg)
+
+    def one_step():
+        ok = 0
+        secs = 0.0
+        for s in sizes:
+            out = TrialOut()
+            assert L.orc_bench_trial(oh.h, sample, s, None, 1, threads, 7, C.byref(out)) == 0
+            ok += out.ok_allocs
+            secs += (out.alloc_ms[0] + out.free_ms[0]) / 1e3
+        return ok, secs
+
+    for _ in range(args.warmup):
+        one_step()
+    tot_ok, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        ok, s = one_step()
+        tot_ok += ok
+        tot_s += s
+    value = tot_ok / tot_s
+    line = {
+        "metric": "malloc+free pairs/s (successful), size sweep",
+        "impl": "reference", "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
+        "data": "synthetic", "config": {"workload": desc, "sample_threads_per_size": sample,
+                                        "sizes": sizes},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "sample": f"{sample} slots per size x {len(sizes)} sizes per step (oracle/ouro_oracle.cpp)"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline(cfgname):
+    """Oracle port timed on the host cores: 2^20 slots x malloc(16) / free,
+    second iteration (mean_subsequent)."""
+    from oracle_lib import OHeap, TrialOut, oracle
+    from paper_2504_18211_b200._abi import Config
+    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    threads = os.cpu_count() or 1
+    cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
+    oh = OHeap(cfg)
+    size = 16
+    ok, secs, iters, verified = 0, 0.0, 0, True
+    t_end = time.perf_counter() + 10.0      # ~10 s of CPU work
+    while time.perf_counter() < t_end and iters < 200:
+        out = TrialOut()
+        assert oracle().orc_bench_trial(oh.h, n, size, None, 4, threads, 7, C.byref(out)) == 0
+        for i in range(1, 4):               # mean_subsequent: first iteration of each trial excluded
+            secs += (out.alloc_ms[i] + out.free_ms[i]) / 1e3
+        ok += out.ok_allocs * 3 // 4
+        iters += 3
+        verified = verified and bool(out.verified)
+    oh.close()
+    return {"value": ok / secs, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "sample": f"{n} slots x malloc({size})/free, {iters} timed iterations (~10 s), "
+                      f"oracle/ouro_oracle.cpp on std::thread x {threads}", "verified": verified}
+
+
+# ------------------------------------------------------------------ GPU ----
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, args.config)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_18211_b200 as ob
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc, kind, flavor, heap_bytes, n, sizes = CONFIGS[args.config]
+    hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
+    heap = ob.Heap(hc, local)
+    ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+    res = torch.zeros(4, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # roofline denominators measured on this device
+    p_same = ob.atomic_peak(local, 2)      # same-address RMW, one per warp
+    p_dist = ob.atomic_peak(local, 0)      # distinct-address 32-bit RMW, one per sector
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    per = {s: {"alloc_ms": [], "free_ms": [], "ok": [], "verify_bad": 0} for s in sizes}
+    launches = 0
+
+    def one_step(record):
+        nonlocal launches
+        for s in sizes:
+            res.zero_()
+            res[1] = -1
+            flush.fill_(1)
+            ev[0].record()
+            heap.launch_alloc(n, ptrs, size=s)
+            ev[1].record()
+            heap.launch_count(n, ptrs, res[2:3])
+            heap.launch_write(n, ptrs, 99, 0)
+            heap.launch_verify(n, ptrs, 99, 0, res)
+            flush.fill_(2)
+            ev[2].record()
+            heap.launch_free(n, ptrs)
+            ev[3].record()
+            ev[3].synchronize()
+            if record:
+                launches += 2
+                p = per[s]
+                p["alloc_ms"].append(ev[0].elapsed_time(ev[1]))
+                p["free_ms"].append(ev[2].elapsed_time(ev[3]))
+                p["ok"].append(int(res[2]))
+                p["verify_bad"] += int(res[0])
+
+    for _ in range(args.warmup):
+        one_step(False)
+    barrier()
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(True)
+        barrier()
+        wall = time.perf_counter() - t0
+    err = heap.last_error()
+    tot_ms = sum(sum(p["alloc_ms"]) + sum(p["free_ms"]) for p in per.values())
+    tot_ok = sum(sum(p["ok"]) for p in per.values())
+    t = torch.tensor([tot_ms, float(tot_ok)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_job, ok_job = float(tmax[0]), float(tsum[1])
+    else:
+        ms_job, ok_job = tot_ms, float(tot_ok)
+    value = ok_job / (ms_job / 1e3)
+
+    # ---------------- e2e through the public C-ABI with host buffers ----------------
+    e2e_ms, e2e_ok = 0.0, 0
+    h_sizes = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    h_res = torch.empty(1, dtype=torch.int64, pin_memory=True)
+    d_sizes = torch.empty(n, dtype=torch.int32, device="cuda")
+    for s in sizes:
+        h_sizes.fill_(s)
+        res.zero_()
+        torch.cuda.synchronize()
+        ev[0].record()
+        d_sizes.copy_(h_sizes, non_blocking=True)          # H2D: this step's requests
+        heap.launch_alloc(n, ptrs, sizes=d_sizes)
+        heap.launch_count(n, ptrs, res[2:3])
+        heap.launch_free(n, ptrs)
+        h_res.copy_(res[2:3], non_blocking=True)             # D2H: the step's result
+        ev[1].record()
+        ev[1].synchronize()
+        e2e_ms += ev[0].elapsed_time(ev[1])
+        e2e_ok += int(h_res[0])
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel ----------------
+    a_ms = sum(sum(p["alloc_ms"]) for p in per.values())
+    f_ms = sum(sum(p["free_ms"]) for p in per.values())
+    dom = "alloc" if a_ms >= f_ms else "free"
+    dom_ms = max(a_ms, f_ms)
+    # binding resource: the per-class queue counters (count + head for alloc,
+    # count + tail for free), each one serial RMW per warp group = ceil(ok/32)
+    chain_ops = sum(sum((o + 31) // 32 for o in p["ok"]) for p in per.values())
+    achieved = chain_ops / (dom_ms / 1e3)
+    per_size = {}
+    for s, p in per.items():
+        am, fm = statistics.mean(p["alloc_ms"]), statistics.mean(p["free_ms"])
+        ok = statistics.mean(p["ok"])
+        per_size[str(s)] = {"ok": int(ok), "oom": n - int(ok), "alloc_us": round(am * 1e3, 2),
+                            "free_us": round(fm * 1e3, 2), "pairs_per_s": ok / ((am + fm) / 1e3)}
+    band = [s for s in sizes if HEADLINE_RANGE[0] <= s <= HEADLINE_RANGE[1]]
+    band_ok = sum(sum(per[s]["ok"]) for s in band)
+    band_ms = sum(sum(per[s]["alloc_ms"]) + sum(per[s]["free_ms"]) for s in band)
+    full = [s for s in sizes if per_size[str(s)]["oom"] == 0]
+    full_ok = sum(sum(per[s]["ok"]) for s in full)
+    full_ms = sum(sum(per[s]["alloc_ms"]) + sum(per[s]["free_ms"]) for s in full)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config)
+        except Exception as e:  # reported, not fatal
+            cpu = {"error": str(e)}
+    line = {
+        "metric": "malloc+free pairs/s (successful), size sweep; % of L2-atomic roofline",
+        "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_job / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64 (integer allocator; no floating point)",
+        "data": "synthetic",
+        "config": {"workload": desc, "variant": ob.variant_name(hc.variant), "heap_bytes": heap_bytes,
+                   "threads": n, "sizes": sizes, "l2": "flushed (256 MiB write) before every timed kernel",
+                   "timed": "alloc kernel + free kernel per size, CUDA events, default stream",
+                   "per_size": per_size,
+                   "pairs_per_s_16B_1KiB": band_ok / (band_ms / 1e3) if band_ms else None,
+                   "pairs_per_s_sizes_without_oom": full_ok / (full_ms / 1e3) if full_ms else None,
+                   "sizes_without_oom": full,
+                   "verify_mismatched_words": sum(p["verify_bad"] for p in per.values()),
+                   "sticky_error": err[0], "wall_s_timed": wall},
+        "roofline": {"bound": "l2_atomic", "kernel": dom,
+                     "resource": "same-address RMW chain on the class-queue counters (1 per warp group)",
+                     "achieved": achieved / 1e9, "peak": p_same / 1e9, "unit": "Gop/s",
+                     "frac": achieved / p_same, "traffic": None,
+                     "peak_source": "measured in-run: ouro_atomic_peak mode 2 (same-address atomicAdd, one per warp)",
+                     "distinct_address_peak_gops": p_dist / 1e9,
+                     "dominant_kernel_share": dom_ms / (a_ms + f_ms)},
+        "e2e": {"value": e2e_ok / (e2e_ms / 1e3) * world, "unit": "pairs/s",
+                "h2d_bytes_per_step": 4 * n * len(sizes), "d2h_bytes_per_step": 8 * len(sizes),
+                "path": "ouro_launch_alloc/count/free (C-ABI) with host-pinned request sizes copied H2D "
+                        "and the success count copied D2H inside the timed region"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -158,8 +158,10 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 
 // ------------------------------------------------------- count / tickets ----
 // Count reservation (broker-queue style).
-__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor) {
-    if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) return 0;  // pre-check, no RMW when empty
+// `precheck`: read the count first and skip the RMW when it is already empty
+// (retries and chunk-queue probes); the reservation result is the same either way.
+__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, bool precheck = true) {
+    if (precheck && (i64)ld_rlx((const u64*)&Q->count) - floor <= 0) return 0;
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
@@ -167,7 +169,6 @@ __device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor) 
     return got;
 }
 __device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
-    if ((i64)ld_rlx((const u64*)&Q->count) + (i64)n > (i64)Q->cap) return false;
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)n);
     if (old + (i64)n > (i64)Q->cap) { atomicAdd((u64*)&Q->count, (u64)(-(i64)n)); return false; }
     return true;
@@ -222,12 +223,12 @@ __device__ __forceinline__ bool arr_enqueue(const ouro_heap_view& v, ouro_queue_
 // Warp-collective Array dequeue for the lanes of `todo`: returns how many were
 // served; the `got` lowest-ranked lanes of todo get *val (NONE on timeout).
 __device__ __forceinline__ u32 arr_dequeue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
-                                           u32 lane, u32 todo, i64 floor, u32* val) {
+                                           u32 lane, u32 todo, i64 floor, u32* val, bool precheck = true) {
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor);
+        got = reserve_deq(Q, n, floor, precheck);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -488,14 +489,14 @@ __device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 m
 // Warp-collective dequeue for the lanes of `todo` (all on queue `qi`).
 template <int FL>
 __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 todo,
-                                         i64 floor, u32* val) {
+                                         i64 floor, u32* val, bool precheck = true) {
     ouro_queue_dev* Q = v.q + qi;
-    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val);
+    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val, precheck);
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor);
+        got = reserve_deq(Q, n, floor, precheck);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -624,10 +625,12 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                                          void** res, int* st) {
     u32 todo = gm, attempt = 0;
     const u32 lt = lanemask_lt();
+    const u32 gl0 = __ffs(gm) - 1;
+    u64 retries = 0;
     while (todo) {
-        const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
+        const u32 rank = __popc(todo & lt);
         u32 h = NONE;
-        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h);
+        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h, attempt > 0);
         const bool mine = ((todo >> lane) & 1u) && rank < got;
         bool ok = mine && h != NONE;
         u32 c = 0, p = 0;
@@ -657,15 +660,15 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         }
         todo = drop_lowest(todo, got);
         if (!todo) break;
-        if (lane == leader) atomicAdd(&v.ctr[k], (u64)__popc(todo));
+        retries += (u64)__popc(todo);
         if (++attempt >= v.max_retries) {
-            if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)__popc(todo));
+            if (lane == gl0) atomicAdd(&v.ctr[v.K + k], (u64)__popc(todo));
             if ((todo >> lane) & 1u) *st = OURO_ERR_OOM;
             break;
         }
         backoff(v, attempt);
-        (void)n;
     }
+    if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);  // one update per call, not per round
 }
 
 // Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).
@@ -677,6 +680,8 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     const u32 ppc = ppc_of(v, k);
     const u32 L = __popc(mask), li = __popc(mask & lt);
     const u32 pool = v.K;
+    const u32 gl0 = __ffs(gm) - 1;
+    u64 retries = 0;
     while (todo) {
         const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
         const bool intodo = (todo >> lane) & 1u;
@@ -755,7 +760,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             todo = drop_lowest(todo, take);
             continue;
         }
-        if (lane == leader) atomicAdd(&v.ctr[k], (u64)n);
+        retries += n;
         if (++attempt >= v.max_retries) {
             if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)n);
             if (intodo) *st = OURO_ERR_OOM;
@@ -763,6 +768,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         }
         backoff(v, attempt);
     }
+    if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);
 }
 
 // malloc for the converged lanes of the calling warp.
@@ -854,7 +860,11 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
     const u32 cgl = __ffs(cg) - 1;
     const bool cl = valid && lane == cgl;
     u64 oldm = 0;
-    if (cl) oldm = atomicAdd(v.meta + c, (u64)__popc(cg));
+    if (KIND == KIND_CHUNK) {
+        if (cl) oldm = atomicAdd(v.meta + c, (u64)__popc(cg));
+    } else {
+        if (cl) atomicAdd(v.meta + c, (u64)__popc(cg));  // result unused: fire-and-forget RED
+    }
     const u32 oldfree = m_free(oldm), newfree = oldfree + (u32)__popc(cg), gen = m_gen(oldm);
     if (KIND == KIND_CHUNK) {
         const u32 ppc = ppc_of(v, k);

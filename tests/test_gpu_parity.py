@@ -45,7 +45,7 @@ def _script_parity(c, steps):
     assert gd == od
     gs, os_ = h.stats(), oh.stats()
     for k in range(gs.num_classes):
-        for f in ("chunks", "live_pages", "queue_len", "queued_live", "seg_live", "seg_hwm", "ooms"):
+        for f in ("chunks", "live_pages", "queue_len", "queued_live", "seg_live", "seg_hwm", "ooms", "retries"):
             assert getattr(gs.cls[k], f) == getattr(os_.cls[k], f), (k, f)
     assert (gs.double_frees, gs.invalid_frees, gs.bad_sizes, gs.stale_drops) == \
         (os_.double_frees, os_.invalid_frees, os_.bad_sizes, os_.stale_drops)
