@@ -255,15 +255,21 @@ def main():
                 p["ok"].append(int(res[2]))
                 p["verify_bad"] += int(res[0])
 
-    for _ in range(args.warmup):
-        one_step(False)
-    barrier()
     with ClockSampler(local) as clk:
+        deadline = time.time() + 3.0
+        while not clk.lines and time.time() < deadline:   # sampler running before any timing
+            time.sleep(0.05)
+        for _ in range(args.warmup):
+            one_step(False)
+        barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             one_step(True)
         barrier()
         wall = time.perf_counter() - t0
+        while time.perf_counter() - t0 < 0.3:              # at least a few samples under load
+            one_step(False)
+        barrier()
     err = heap.last_error()
     tot_ms = sum(sum(p["alloc_ms"]) + sum(p["free_ms"]) for p in per.values())
     tot_ok = sum(sum(p["ok"]) for p in per.values())

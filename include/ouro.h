@@ -171,6 +171,9 @@ ouro_status ouro_heap_reset(ouro_heap* heap, void* stream);
 /* Copy the POD device view (struct ouro_heap_view in ouro_device.cuh). */
 ouro_status ouro_heap_get_view(const ouro_heap* heap, void* view_out, size_t view_size);
 size_t ouro_heap_view_size(void);
+/* Debug mode: verify queue/bitmap invariants on every device op (CorruptionError
+ * on mismatch).  Off by default; affects views fetched afterwards. */
+ouro_status ouro_heap_set_checks(ouro_heap* heap, int on);
 ouro_status ouro_heap_config(const ouro_heap* heap, ouro_config* cfg, ouro_geometry* geo);
 uint64_t ouro_heap_base(const ouro_heap* heap); /* device address of heap byte 0 */
 /* page_region against live device state; InvalidHandle if the

@@ -82,7 +82,12 @@ typedef struct ouro_heap_view {
     uint32_t Wmax, gmask, cmask;
     uint32_t kind, flavor, backoff;
     uint32_t max_retries, sleep_base_ns, sleep_cap_ns;
-    uint32_t reserved0;
+    uint32_t checks;        /* 1: verify queue/bitmap invariants on every op (debug) */
+    /* page kind static partition: class k owns chunks
+     * [start_k, start_k + n_k), the first s_k of them segment storage (gap G1);
+     * n_0 = pq_n0, n_k = pq_q for k > 0, so decode is arithmetic, not a load. */
+    uint32_t pq_n0, pq_q;
+    uint32_t pq_s[32];
 } ouro_heap_view;
 
 #endif

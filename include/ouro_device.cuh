@@ -86,21 +86,10 @@ __device__ __forceinline__ void ballot_scan8(u32 mask, u32 v, u32 lt, u32* pre, 
     *tot = t;
 }
 
-// the mask `todo` minus its `k` lowest set bits
-__device__ __forceinline__ u32 drop_lowest(u32 todo, u32 k) {
-    for (u32 i = 0; i < k && todo; ++i) todo &= todo - 1;
-    return todo;
-}
-
 __device__ __forceinline__ u32 nth_set64(u64 b, u32 x) {
     for (u32 i = 0; i < x; ++i) b &= b - 1;
     return (u32)(__ffsll((long long)b) - 1);
 }
-
-struct View {
-    const ouro_heap_view& v;
-    __device__ explicit View(const ouro_heap_view& x) : v(x) {}
-};
 
 __device__ __forceinline__ void raise_err(const ouro_heap_view& v, int code) {
     atomicCAS(&v.sticky[0], 0u, (u32)code);
@@ -174,6 +163,13 @@ __device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
     return true;
 }
 
+// Enqueue reservation for queues that cannot overflow by construction (page
+// queues hold each page at most once -- the bitmap rejects double frees --
+// and pools hold each chunk at most once): fire-and-forget add, no round trip.
+__device__ __forceinline__ void reserve_enq_nofull(ouro_queue_dev* Q, u32 n) {
+    atomicAdd((u64*)&Q->count, (u64)n);
+}
+
 __device__ __forceinline__ u32 vtag(u64 t) { return ((u32)t & 0x7FFFFFFFu) | 0x80000000u; }
 
 // ---------------------------------------------------------- Array slots ----
@@ -202,15 +198,20 @@ __device__ __forceinline__ bool arr_take(const ouro_heap_view& v, ouro_queue_dev
 // Warp-collective Array enqueue: lanes in `part` (all of one queue) enqueue
 // their value in lane order.  Called by every lane of `mask`.
 __device__ __forceinline__ bool arr_enqueue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
-                                            u32 lane, u32 part, u32 val) {
+                                            u32 lane, u32 part, u32 val, bool nofull = false) {
     if (!part) return true;
     const u32 leader = __ffs(part) - 1, n = __popc(part), rank = __popc(part & lanemask_lt());
     u64 t0 = 0;
     u32 ok = 0;
     if (lane == leader) {
-        Spin sp;
-        while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
-            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        if (nofull) {
+            reserve_enq_nofull(Q, n);
+            ok = 1;
+        } else {
+            Spin sp;
+            while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
+                if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        }
         if (ok) t0 = atomicAdd((u64*)&Q->tail, (u64)n);
     }
     ok = __shfl_sync(mask, ok, leader);
@@ -370,7 +371,7 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
         if (!go) return;
         released = __shfl_sync(mask, released, who);
         if (released) {
-            arr_enqueue(v, v.q + Q->seg_src, mask, lane, 1u << who, ch);
+            arr_enqueue(v, v.q + Q->seg_src, mask, lane, 1u << who, ch, true);
             if (lane == who) seg_count(Q, -1);
         }
     }
@@ -454,17 +455,23 @@ __device__ __forceinline__ bool q_take(const ouro_heap_view& v, ouro_queue_dev* 
 
 // Warp-collective enqueue of the lanes in `part` into queue `qi` (lane order).
 template <int FL>
-__device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 part, u32 val) {
+__device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 part, u32 val,
+                                          bool nofull = false) {
     ouro_queue_dev* Q = v.q + qi;
-    if (FL == FL_ARRAY) return arr_enqueue(v, Q, mask, lane, part, val);
+    if (FL == FL_ARRAY) return arr_enqueue(v, Q, mask, lane, part, val, nofull);
     if (!part) return true;
     const u32 leader = __ffs(part) - 1, n = __popc(part), rank = __popc(part & lanemask_lt());
     u64 t0 = 0;
     u32 ok = 0;
     if (lane == leader) {
-        Spin sp;
-        while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
-            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        if (nofull) {
+            reserve_enq_nofull(Q, n);
+            ok = 1;
+        } else {
+            Spin sp;
+            while (!(ok = reserve_enq(Q, n) ? 1u : 0u))
+                if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); break; }
+        }
         if (ok) t0 = atomicAdd((u64*)&Q->tail, (u64)n);
     }
     ok = __shfl_sync(mask, ok, leader);
@@ -527,7 +534,7 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
         }
         const u32 rm = __ballot_sync(mask, retire);
         if (rm) {
-            arr_enqueue(v, v.q + Q->seg_src, mask, lane, rm, rc);
+            arr_enqueue(v, v.q + Q->seg_src, mask, lane, rm, rc, true);
             if (retire) {
                 __threadfence();
                 st_rel(Q->dir + (s % Q->D), ((u64)(u32)(s + Q->D) << 32) | NONE);
@@ -547,13 +554,14 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
 // queue qi, groups served in order of their lowest lane.
 template <int FL>
 __device__ __forceinline__ void q_enqueue_by_queue(const ouro_heap_view& v, u32 mask, u32 lane, bool part,
-                                                   u32 qi, u32 val) {
+                                                   u32 qi, u32 val, bool nofull = false) {
     u32 pending = __ballot_sync(mask, part);
     while (pending) {
         const u32 leader = __ffs(pending) - 1;
         const u32 gq = __shfl_sync(mask, qi, leader);
         const u32 grp = __ballot_sync(mask, part && ((pending >> lane) & 1u) && qi == gq);
-        if (!q_enqueue<FL>(v, gq, mask, lane, grp, val) && ((grp >> lane) & 1u)) raise_err(v, OURO_ERR_CORRUPTION);
+        if (!q_enqueue<FL>(v, gq, mask, lane, grp, val, nofull) && ((grp >> lane) & 1u))
+            raise_err(v, OURO_ERR_CORRUPTION);
         pending &= ~grp;
     }
 }
@@ -647,8 +655,12 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             const u64 bits = ((u64)hi << 32) | lo;
             const u32 gl = __ffs(grp) - 1;
             if (ok && lane == gl) {
-                const u64 old = atomicAnd(wp, ~bits);
-                if ((old & bits) != bits) raise_err(v, OURO_ERR_CORRUPTION);
+                if (v.checks) {
+                    const u64 old = atomicAnd(wp, ~bits);
+                    if ((old & bits) != bits) raise_err(v, OURO_ERR_CORRUPTION);
+                } else {
+                    atomicAnd(wp, ~bits);  // result unused: RED
+                }
             }
             // free_count -= pages taken, one add per distinct chunk
             const u32 cg = __match_any_sync(mask, ok ? (u64)c : (~0ull - lane));
@@ -658,7 +670,7 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                 else *st = OURO_ERR_TIMEOUT;
             }
         }
-        todo = drop_lowest(todo, got);
+        todo &= ~__ballot_sync(mask, mine);
         if (!todo) break;
         retries += (u64)__popc(todo);
         if (++attempt >= v.max_retries) {
@@ -717,7 +729,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                     *st = OURO_ERR_CORRUPTION;
                 }
             }
-            todo = drop_lowest(todo, take);
+            todo &= ~__ballot_sync(mask, intodo && rank < take);
             continue;
         }
         u32 c = NONE;
@@ -757,7 +769,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                 *res = v.base + ((u64)c << v.chunk_shift) + ((u64)rank << (v.min_shift + k));
                 *st = OURO_OK;
             }
-            todo = drop_lowest(todo, take);
+            todo &= ~__ballot_sync(mask, intodo && rank < take);
             continue;
         }
         retries += n;
@@ -815,7 +827,15 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
             st = OURO_ERR_INVALID_HANDLE;
         } else {
             c = (u32)(off >> v.chunk_shift);
-            const u32 s8 = m_state(ld_rlx(v.meta + c));
+            u32 s8;
+            if (KIND == KIND_PAGE) {
+                // static partition: class and Reserved-ness are arithmetic (no meta load)
+                const u32 kk = c < v.pq_n0 ? 0u : 1u + (c - v.pq_n0) / v.pq_q;
+                const u32 start = kk == 0 ? 0u : v.pq_n0 + (kk - 1) * v.pq_q;
+                s8 = (kk >= v.K) ? 0u : ((c - start < v.pq_s[kk]) ? ST_RESERVED : kk + 1);
+            } else {
+                s8 = m_state(ld_rlx(v.meta + c));
+            }
             if (s8 == ST_UNASSIGNED || s8 == ST_RESERVED || s8 > v.K) {
                 st = OURO_ERR_INVALID_HANDLE;
             } else {
@@ -905,12 +925,12 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
             }
             __threadfence();
             __syncwarp(mask);
-            arr_enqueue(v, v.q + v.K, mask, lane, cm, c);  // return to pool
+            arr_enqueue(v, v.q + v.K, mask, lane, cm, c, true);  // return to pool
         }
         // 0 -> >0: the releaser re-enqueues the chunk
         q_enqueue_by_queue<FL>(v, mask, lane, cl && oldfree == 0 && !closed, k, q_entry(v, c, gen));
     } else {
-        q_enqueue_by_queue<FL>(v, mask, lane, valid, k, (c << v.page_bits) | pi);
+        q_enqueue_by_queue<FL>(v, mask, lane, valid, k, (c << v.page_bits) | pi, true);
     }
     return st;
 }

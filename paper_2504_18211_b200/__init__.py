@@ -72,6 +72,7 @@ def _declare(L):
         "ouro_heap_reset": (i32, [P, P]),
         "ouro_heap_get_view": (i32, [P, P, C.c_size_t]),
         "ouro_heap_view_size": (C.c_size_t, []),
+        "ouro_heap_set_checks": (i32, [P, C.c_int]),
         "ouro_heap_config": (i32, [P, C.POINTER(Config), C.POINTER(Geometry)]),
         "ouro_heap_base": (u64, [P]),
         "ouro_page_region": (i32, [P, u32, C.POINTER(u64), C.POINTER(u64)]),
@@ -301,6 +302,10 @@ class Heap:
     @property
     def handle(self):
         return self._h
+
+    def set_checks(self, on: bool = True):
+        """Debug mode: verify queue/bitmap invariants on every device op."""
+        check(lib().ouro_heap_set_checks(self._h, int(on)), "set_checks")
 
     def reset(self, stream=None):
         check(lib().ouro_heap_reset(self._h, _stream(stream)), "reset")

@@ -646,6 +646,12 @@ void make_view(ouro_heap* H) {
     v.max_retries = H->cfg.max_retries;
     v.sleep_base_ns = H->cfg.sleep_base_ns;
     v.sleep_cap_ns = H->cfg.sleep_cap_ns;
+    v.checks = 0;
+    if (H->cfg.allocator_kind == OURO_KIND_PAGE) {
+        v.pq_n0 = H->pq_n.empty() ? g.N : H->pq_n[0];
+        v.pq_q = g.N / g.K;
+        for (u32 k = 0; k < g.K && k < 32; ++k) v.pq_s[k] = H->pq_s[k];
+    }
 }
 
 // Quiescent canonical digest + per-class recount (device passes, host finish).
@@ -845,6 +851,12 @@ ouro_status ouro_heap_reset(ouro_heap* H, void* stream) {
 }
 
 size_t ouro_heap_view_size(void) { return sizeof(ouro_heap_view); }
+
+ouro_status ouro_heap_set_checks(ouro_heap* H, int on) {
+    if (!H) return OURO_ERR_USAGE;
+    H->view.checks = on ? 1u : 0u;
+    return OURO_OK;
+}
 
 ouro_status ouro_heap_get_view(const ouro_heap* H, void* out, size_t size) {
     if (!H || !out || size < sizeof(ouro_heap_view)) return OURO_ERR_USAGE;

@@ -20,11 +20,13 @@ pytestmark = pytest.mark.gpu
 IDS = [NAMES[v] for v in VARIANTS]
 
 
-def _heap(c):
+def _heap(c, checks=True):
     hc = ob.HeapConfig(c.heap_bytes, c.chunk_bytes, c.min_page_bytes, c.max_page_bytes,
                        ob.QueueFlavor(c.queue_flavor), ob.AllocatorKind(c.allocator_kind),
                        ob.BackoffPolicy(c.backoff), c.max_retries)
-    return ob.Heap(hc, 0)
+    h = ob.Heap(hc, 0)
+    h.set_checks(checks)
+    return h
 
 
 def _script_parity(c, steps):
@@ -126,7 +128,7 @@ def test_concurrent_phased(cuda, variant, size):
     c = cfg(kind, flavor, _heap_bytes(kind), retries=64)
     n = 65536 if size <= 1000 else 8192
     want_ok, want_digest = _oracle_run(c, [size] * n)
-    h = _heap(c)
+    h = _heap(c, checks=(size != 1000))  # size 1000 runs the production (unchecked) path
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
     for it in range(3):
         res = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
