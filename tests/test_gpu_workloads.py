@@ -1,0 +1,208 @@
+"""GPU workloads through the C-ABI beyond op-script parity: the paper's driver
+(run_trial), mixed churn (BASELINE configs[3]), OOM resilience, error paths at
+scale, virtual-queue segment stress, and the BASELINE-sized heaps."""
+import pytest
+
+import paper_2504_18211_b200 as ob
+from helpers import NAMES, VARIANTS
+from oracle_lib import OHeap
+
+pytestmark = pytest.mark.gpu
+IDS = [NAMES[v] for v in VARIANTS]
+
+
+def _hc(kind, flavor, heap, chunk=64 << 10, maxp=8192, retries=64, backoff=0):
+    return ob.HeapConfig(heap, chunk, 16, maxp, ob.QueueFlavor(flavor), ob.AllocatorKind(kind),
+                         ob.BackoffPolicy(backoff), retries)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_run_trial_paper_driver(cuda, variant):
+    """SPEC.md:385 (PAPER): 1024 allocations x 1000 B x 10 iterations -> Pass,
+    mean_subsequent over iterations 2..10."""
+    with ob.Heap(_hc(*variant, 64 << 20)) as h:
+        r = h.run_trial(1024, 1000, iterations=10, seed=3)
+        assert r.verified == 1 and r.ok_allocs == 10240 and r.failed_allocs == 0
+        assert r.mean_subsequent_ms == pytest.approx(sum(r.alloc_ms[1:10]) / 9)
+        assert r.mean_all_ms == pytest.approx(sum(r.alloc_ms[:10]) / 10)
+        assert h.last_error()[0] == 0
+        d = h.digest()
+        assert d.live_pages == 0 and d.partition_ok == 1
+
+
+def test_run_trial_with_host_sizes(cuda):
+    with ob.Heap(_hc(1, 0, 256 << 20)) as h:
+        sizes = [(i * 37) % 4000 + 1 for i in range(20000)]
+        r = h.run_trial(len(sizes), sizes=sizes, iterations=3)
+        assert r.verified == 1 and r.ok_allocs == 3 * len(sizes) and r.h2d_bytes == 4 * len(sizes)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_oom_resilience(cuda, variant):
+    """Criterion 8: a trial demanding more than capacity fails
+    without aborting, and a normal trial afterwards passes."""
+    torch = cuda
+    kind, flavor = variant
+    with ob.Heap(_hc(kind, flavor, 16 << 20, retries=8)) as h:
+        n = 1 << 16
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        h.launch_alloc(n, ptrs, size=4096)          # 256 MiB demand into a 16 MiB heap
+        h.launch_count(n, ptrs, cnt)
+        torch.cuda.synchronize()
+        ok = int(cnt)
+        assert 0 < ok < n
+        a = h.audit(n, ptrs)
+        assert a.live == ok and a.overlaps == 0 and a.out_of_heap == 0 and a.misaligned == 0
+        s = h.stats()
+        assert sum(s.cls[k].ooms for k in range(s.num_classes)) == n - ok
+        h.launch_free(n, ptrs)
+        torch.cuda.synchronize()
+        r = h.run_trial(1024, 100, iterations=2)
+        assert r.verified == 1 and r.failed_allocs == 0
+        assert h.last_error()[0] == 0
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_double_free_at_scale(cuda, variant):
+    """DoubleFree is surfaced, never silently ignored (errors.hpp:22-27): free
+    every pointer twice from 65 536 threads."""
+    torch = cuda
+    with ob.Heap(_hc(*variant, 64 << 20)) as h:
+        n = 1 << 16
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        h.launch_alloc(n, ptrs, size=48)
+        h.launch_free(n, ptrs)
+        h.launch_free(n, ptrs)
+        torch.cuda.synchronize()
+        s = h.stats()
+        assert s.double_frees == n and s.invalid_frees == 0
+        first, mask = h.last_error(clear=True)
+        assert first == ob._abi.ERR_DOUBLE_FREE and mask == 1 << ob._abi.ERR_DOUBLE_FREE
+        d = h.digest()
+        assert d.live_pages == 0 and d.partition_ok == 1
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_invalid_frees_at_scale(cuda, variant):
+    torch = cuda
+    with ob.Heap(_hc(*variant, 64 << 20)) as h:
+        n = 1 << 15
+        base = h.base
+        bogus = torch.arange(n, dtype=torch.int64, device="cuda") * 64 + base + 8   # misaligned
+        h.launch_free(n, bogus)
+        out = torch.full((n,), base + (64 << 20) + 4096, dtype=torch.int64, device="cuda")  # outside
+        h.launch_free(n, out)
+        torch.cuda.synchronize()
+        s = h.stats()
+        assert s.invalid_frees == 2 * n and s.double_frees == 0
+        h.last_error(clear=True)
+        d = h.digest()
+        assert d.live_pages == 0 and d.partition_ok == 1
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_churn(cuda, variant):
+    """BASELINE configs[3] shape (scaled): mixed sizes 8 B-4 KiB, interleaved
+    alloc/free rounds in one kernel per round; stamps checked every round;
+    free-all restores the canonical state the oracle reaches."""
+    torch = cuda
+    kind, flavor = variant
+    heap = 1 << 30
+    n = 1 << 18
+    with ob.Heap(_hc(kind, flavor, heap)) as h:
+        slots = torch.zeros(n, dtype=torch.int64, device="cuda")
+        res = torch.zeros(5, dtype=torch.int64, device="cuda")
+        h.launch_churn(n, 0, 20, 1, slots, res)
+        torch.cuda.synchronize()
+        ok, failed, frees, reused, bad = [int(x) for x in res]
+        assert bad == 0 and ok > 0 and frees > 0 and reused > 0
+        a = h.audit(n, slots)
+        assert a.overlaps == 0 and a.out_of_heap == 0 and a.misaligned == 0 and a.not_marked == 0
+        h.launch_free(n, slots)
+        torch.cuda.synchronize()
+        assert h.last_error()[0] == 0
+        d = h.digest().as_dict()
+        assert d["live_pages"] == 0 and d["partition_ok"] == 1
+        if kind == 0:
+            oh = OHeap(_hc(kind, flavor, heap).to_c())
+            assert d == oh.digest().as_dict()     # page kind: back to the exact initial state
+            oh.close()
+        else:
+            # chunk kind: exactly one retained chunk per class ever used (8 B-4 KiB -> classes 0..8)
+            assert d["class_chunks"][:9] == [1] * 9 and d["class_chunks"][9] == 0
+
+
+@pytest.mark.parametrize("flavor", [1, 2])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_virtual_segment_stress(cuda, kind, flavor):
+    """Tiny chunks (1 KiB -> 128 / 126-slot segments): 2^18 threads create and
+    retire thousands of segments concurrently; audit + digest must stay exact."""
+    torch = cuda
+    hc = _hc(kind, flavor, 64 << 20, chunk=1024, maxp=1024)
+    want = None
+    n = 1 << 18
+    with ob.Heap(hc) as h:
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for it in range(3):
+            cnt.zero_()
+            h.launch_alloc(n, ptrs, size=64)
+            h.launch_count(n, ptrs, cnt)
+            torch.cuda.synchronize()
+            a = h.audit(n, ptrs)
+            assert a.live == int(cnt) and a.overlaps == 0 and a.not_marked == 0
+            if want is None:
+                want = int(cnt)
+            h.launch_free(n, ptrs)
+            torch.cuda.synchronize()
+        assert h.last_error()[0] == 0
+        s = h.stats()
+        assert s.timeouts == 0 and s.corruptions == 0
+        assert max(s.cls[k].seg_hwm for k in range(s.num_classes)) > 10
+        d = h.digest()
+        assert d.partition_ok == 1 and d.live_pages == 0
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_sleep_backoff(cuda, variant):
+    """SleepRetry: nanosleep(min(base*2^a, cap)) between rounds."""
+    torch = cuda
+    with ob.Heap(_hc(*variant, 16 << 20, retries=6, backoff=1)) as h:
+        n = 1 << 15
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        h.launch_alloc(n, ptrs, size=8192)
+        h.launch_free(n, ptrs)
+        torch.cuda.synchronize()
+        assert h.last_error()[0] == 0
+        assert h.digest().live_pages == 0
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_baseline_heaps_1m_threads(cuda, variant):
+    """BASELINE configs[1]/[2] sizes: 2^20 threads on a 1 GiB (Array) / 8 GiB
+    (virtual) heap, 16 B and 512 B; audit + verify + canonical free-all."""
+    torch = cuda
+    kind, flavor = variant
+    heap = (1 << 30) if flavor == 0 else (8 << 30)
+    n = 1 << 20
+    with ob.Heap(_hc(kind, flavor, heap)) as h:
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        for size in (16, 512):
+            res = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
+            h.launch_alloc(n, ptrs, size=size)
+            h.launch_count(n, ptrs, res[2:3])
+            h.launch_write(n, ptrs, 5, size)
+            h.launch_verify(n, ptrs, 5, size, res)
+            torch.cuda.synchronize()
+            ok = int(res[2])
+            if flavor != 0 or size == 16 or kind == 1:
+                assert ok == n, (size, ok)
+            assert int(res[0]) == 0
+            a = h.audit(n, ptrs)
+            assert a.live == ok and a.overlaps == 0 and a.not_marked == 0
+            h.launch_free(n, ptrs)
+            torch.cuda.synchronize()
+        assert h.last_error()[0] == 0
+        d = h.digest()
+        assert d.live_pages == 0 and d.partition_ok == 1
