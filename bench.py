@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--config", default="pq1g", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-threads", type=int, default=0)
+    ap.add_argument("--sizes", default="", help="comma list overriding the config's sweep (experiments)")
     return ap.parse_args()
 
 
@@ -210,6 +211,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     desc, kind, flavor, heap_bytes, n, sizes = CONFIGS[args.config]
+    if args.sizes:
+        sizes = [int(x) for x in args.sizes.split(",")]
     hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
     heap = ob.Heap(hc, local)
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")

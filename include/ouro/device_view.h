@@ -5,7 +5,8 @@
  * HBM layout of one heap:
  *   payload      heap_bytes, chunk c at base + c*chunk_bytes
  *   meta[N]      u64 per chunk: {free:32 | state:8 | gen:24}      (ChunkHeader)
- *   bitmap[N*W]  u64 words, 1 = free page
+ *   bitmap[N*W]  u64 words, 1 = allocated page (SPEC.md:185 with the bit sense
+ *                inverted: unassigned / fully free chunks are all-zero)
  *   queues[2K+1] ouro_queue_dev: K class queues, the chunk pool, K private
  *                segment pools (page kind, virtual flavours)
  *   slots        Array-flavour rings, u64 {tag:32 | value:32}

@@ -108,15 +108,29 @@ struct Spin {
     }
 };
 
-// backoff: FenceRetry = device fence; SleepRetry =
-// nanosleep(min(base * 2^attempt, cap)).
+// backoff: FenceRetry = fence + yield (no sleep);
+// SleepRetry = nanosleep(min(base * 2^attempt, cap)).
+// The retry poll is a .relaxed.gpu load of the queue count, served by L2, so it
+// observes every other SM's frees without any fence; a device-scope fence
+// (fence.sc/acq_rel.gpu -> MEMBAR.GPU + ERRBAR + CCTL.IVALL, measured ~2.5 us
+// per round on B200) would only add delay.  The default therefore fences at CTA
+// scope (orders this warp's own accesses) and yields; build with
+// -DOURO_FENCE_SCOPE_GPU=1 for the literal device-wide seq-cst fence.
+#ifndef OURO_FENCE_SCOPE_GPU
+#define OURO_FENCE_SCOPE_GPU 0
+#endif
 __device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
     if (v.backoff == OURO_BACKOFF_SLEEP) {
         u64 ns = attempt >= 40 ? v.sleep_cap_ns : ((u64)v.sleep_base_ns << attempt);
         if (ns > v.sleep_cap_ns) ns = v.sleep_cap_ns;
         __nanosleep((u32)ns);
     } else {
-        __threadfence();
+#if OURO_FENCE_SCOPE_GPU
+        asm volatile("fence.sc.gpu;" ::: "memory");
+#else
+        asm volatile("fence.sc.cta;" ::: "memory");
+#endif
+        __nanosleep(0);
     }
 }
 
@@ -146,11 +160,57 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 }
 
 // ------------------------------------------------------- count / tickets ----
+// Per-block poll combining for retry rounds.  Retrying warps (OOM storms:
+// ~10^6 lanes x max_retries rounds) would otherwise all poll the same count
+// word, and same-address loads serialise in one L2 slice.  Within a block, the
+// first warp to need a fresh observation of a queue becomes the poller (CAS on
+// a shared-memory entry marked in-flight), the others wait (bounded) for its
+// result.  The result is at most kPollWindow old, i.e. equivalent to having
+// polled that much earlier; a non-empty result still goes through the
+// authoritative reservation RMW.  Entry: [63:8] time/256 ns, [7:2] queue tag,
+// [1] in flight, [0] empty.
+constexpr u64 kPollWindow = 8;  // x 256 ns
+__device__ __forceinline__ u64 gtime256() {
+    u64 t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t >> 8;
+}
+__device__ __forceinline__ u64* poll_cache() {
+    __shared__ u64 cache[8];
+    return cache;
+}
+// true: the queue was observed (count - floor <= 0) within the window
+__device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
+    const u64 tag = (((u64)Q >> 10) ^ ((u64)Q >> 16)) & 63u;
+    u64* slot = poll_cache() + (tag & 7);
+    for (int spins = 0; spins < 64; ++spins) {
+        const u64 now = gtime256();
+        const u64 e = *reinterpret_cast<volatile u64*>(slot);
+        const bool fresh = ((e >> 2) & 63u) == tag && now - (e >> 8) < kPollWindow;
+        if (fresh && !(e & 2u)) return (e & 1u) != 0;
+        if (fresh) { __nanosleep(32); continue; }  // another warp's poll in flight
+        const u64 mine = (now << 8) | (tag << 2) | 2u;
+        if (atomicCAS(slot, e, mine) != e) continue;
+        const bool empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
+        atomicExch(slot, (gtime256() << 8) | (tag << 2) | (empty ? 1u : 0u));
+        return empty;
+    }
+    return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
+}
+
 // Count reservation (broker-queue style).
 // `precheck`: read the count first and skip the RMW when it is already empty
 // (retries and chunk-queue probes); the reservation result is the same either way.
-__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, bool precheck = true) {
-    if (precheck && (i64)ld_rlx((const u64*)&Q->count) - floor <= 0) return 0;
+// `combine`: take the pre-check from the block's poll combiner (retry rounds).
+__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, bool precheck = true,
+                                           bool combine = false) {
+    if (precheck) {
+        if (combine) {
+            if (observed_empty(Q, floor)) return 0;
+        } else if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
+            return 0;
+        }
+    }
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
@@ -224,12 +284,13 @@ __device__ __forceinline__ bool arr_enqueue(const ouro_heap_view& v, ouro_queue_
 // Warp-collective Array dequeue for the lanes of `todo`: returns how many were
 // served; the `got` lowest-ranked lanes of todo get *val (NONE on timeout).
 __device__ __forceinline__ u32 arr_dequeue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
-                                           u32 lane, u32 todo, i64 floor, u32* val, bool precheck = true) {
+                                           u32 lane, u32 todo, i64 floor, u32* val, bool precheck = true,
+                                           bool combine = false) {
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor, precheck);
+        got = reserve_deq(Q, n, floor, precheck, combine);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -496,14 +557,14 @@ __device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 m
 // Warp-collective dequeue for the lanes of `todo` (all on queue `qi`).
 template <int FL>
 __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 todo,
-                                         i64 floor, u32* val, bool precheck = true) {
+                                         i64 floor, u32* val, bool precheck = true, bool combine = false) {
     ouro_queue_dev* Q = v.q + qi;
-    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val, precheck);
+    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val, precheck, combine);
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor, precheck);
+        got = reserve_deq(Q, n, floor, precheck, combine);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -567,13 +628,15 @@ __device__ __forceinline__ void q_enqueue_by_queue(const ouro_heap_view& v, u32 
 }
 
 // ---------------------------------------------------------- chunk bitmap ----
-// Claim the `take` lowest set bits of chunk c's bitmap.
+// Claim the `take` lowest free pages (clear bits below ppc) of chunk c
+// (lowest free word first, fetch-OR the chosen bits).
 // Each lane of `mask` scans two words per window; the requester of rank
 // `req` (< take, NONE for others) receives the req-th lowest claimed page.
 __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k, u32 take, u32 mask,
                                           u32 lane, u32 req) {
     const u32 L = __popc(mask), lt = lanemask_lt(), li = __popc(mask & lt);
     const u32 W = words_of(v, k);
+    const u32 ppc = ppc_of(v, k);
     u64* row = bm_row(v, c);
     u32 claimed = 0, page = NONE;
     Spin sp;
@@ -587,6 +650,10 @@ __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k,
             } else if (wi < W) {
                 w0 = ld_rlx(row + wi);
             }
+            // free = clear bits below ppc
+            w0 = wi < W ? (~w0 & (ppc - wi * 64 >= 64 ? ~0ull : ((1ull << (ppc - wi * 64)) - 1ull))) : 0ull;
+            w1 = wi + 1 < W ? (~w1 & (ppc - (wi + 1) * 64 >= 64 ? ~0ull : ((1ull << (ppc - (wi + 1) * 64)) - 1ull)))
+                            : 0ull;
             const u32 cnt = (u32)(__popcll((long long)w0) + __popcll((long long)w1));
             u32 pre, tot;
             ballot_scan8(mask, cnt, lt, &pre, &tot);
@@ -596,8 +663,8 @@ __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k,
             for (u64 b = w0; my && b; b &= b - 1, --my) p0 |= b & (~b + 1);
             for (u64 b = w1; my && b; b &= b - 1, --my) p1 |= b & (~b + 1);
             u64 g0 = 0, g1 = 0;
-            if (p0) g0 = atomicAnd(row + wi, ~p0) & p0;
-            if (p1) g1 = atomicAnd(row + wi + 1, ~p1) & p1;
+            if (p0) g0 = ~atomicOr(row + wi, p0) & p0;
+            if (p1) g1 = ~atomicOr(row + wi + 1, p1) & p1;
             if (g0 != p0 || g1 != p1) raise_err(v, OURO_ERR_CORRUPTION);
             const u32 gc = (u32)(__popcll((long long)g0) + __popcll((long long)g1));
             u32 gpre, gtot;
@@ -638,7 +705,7 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     while (todo) {
         const u32 rank = __popc(todo & lt);
         u32 h = NONE;
-        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h, attempt > 0);
+        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h, attempt > 0, attempt > 0);
         const bool mine = ((todo >> lane) & 1u) && rank < got;
         bool ok = mine && h != NONE;
         u32 c = 0, p = 0;
@@ -654,12 +721,12 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             const u32 lo = __reduce_or_sync(grp, (u32)bit), hi = __reduce_or_sync(grp, (u32)(bit >> 32));
             const u64 bits = ((u64)hi << 32) | lo;
             const u32 gl = __ffs(grp) - 1;
-            if (ok && lane == gl) {
+            if (ok && lane == gl) {  // mark the pages allocated
                 if (v.checks) {
-                    const u64 old = atomicAnd(wp, ~bits);
-                    if ((old & bits) != bits) raise_err(v, OURO_ERR_CORRUPTION);
+                    const u64 old = atomicOr(wp, bits);
+                    if (old & bits) raise_err(v, OURO_ERR_CORRUPTION);
                 } else {
-                    atomicAnd(wp, ~bits);  // result unused: RED
+                    atomicOr(wp, bits);  // result unused: RED
                 }
             }
             // free_count -= pages taken, one add per distinct chunk
@@ -690,7 +757,6 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     u32 todo = gm, attempt = 0;
     const u32 lt = lanemask_lt();
     const u32 ppc = ppc_of(v, k);
-    const u32 L = __popc(mask), li = __popc(mask & lt);
     const u32 pool = v.K;
     const u32 gl0 = __ffs(gm) - 1;
     u64 retries = 0;
@@ -698,7 +764,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
         const bool intodo = (todo >> lane) & 1u;
         u32 e = NONE;
-        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e);
+        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, true, attempt > 0);
         e = __shfl_sync(mask, e, leader);
         if (got && e != NONE) {
             const u32 c = e & v.cmask;
@@ -733,7 +799,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             continue;
         }
         u32 c = NONE;
-        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c);
+        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, true, attempt > 0);
         c = __shfl_sync(mask, c, leader);
         if (got && c != NONE) {
             const u32 take = min(n, ppc);
@@ -748,22 +814,19 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                 continue;
             }
             const u32 gen = (m_gen(m) + 1u) & 0xFFFFFFu;
-            // chunk_assign fused with taking pages 0..take-1 (whole warp writes the bitmap)
-            u64* row = bm_row(v, c);
-            const u32 W = words_of(v, k);
-            for (u32 w = li; w < W; w += L) {
-                const u32 lo = w * 64, hi = min(ppc, lo + 64);
-                u64 bits = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1ull);
-                const u32 th = min(take, hi);
-                if (th > lo) { const u32 nt = th - lo; bits &= (nt == 64) ? 0ull : ~((1ull << nt) - 1ull); }
-                st_rlx(row + w, bits);
-            }
-            __threadfence();
-            __syncwarp(mask);
+            // chunk_assign fused with taking pages 0..take-1.  A pool chunk's bitmap
+            // is all-zero (all free), so one fetch-OR marks the taken pages; the
+            // header is published with an exchange issued only after that RMW has
+            // returned (control dependency: both performed at L2, in order), and the
+            // entry is enqueued after the exchange returned -- no device fence.
             if (lane == leader) {
-                st_rel(v.meta + c, mk_meta(gen, k + 1, ppc - take));
+                const u64 tb = (take >= 64) ? ~0ull : ((1ull << take) - 1ull);
+                if (atomicOr(bm_row(v, c), tb) & tb) raise_err(v, OURO_ERR_CORRUPTION);
+                const u64 prev = atomicExch(v.meta + c, mk_meta(gen, k + 1, ppc - take));
+                if (m_state(prev) != ST_UNASSIGNED) raise_err(v, OURO_ERR_CORRUPTION);
                 atomicAdd(v.assigned + k, 1u);
             }
+            __syncwarp(mask);
             q_enqueue<FL>(v, k, mask, lane, (ppc - take > 0) ? (1u << leader) : 0u, q_entry(v, c, gen));
             if (intodo && rank < take) {
                 *res = v.base + ((u64)c << v.chunk_shift) + ((u64)rank << (v.min_shift + k));
@@ -851,7 +914,7 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
         const u32 same = __match_any_sync(mask, valid ? off : (~0ull - lane));
         if (valid && (same & lt)) { valid = false; st = OURO_ERR_DOUBLE_FREE; }
     }
-    // set the page bits, one fetch-OR per distinct word (old bit set => DoubleFree)
+    // clear the allocated bits, one fetch-AND per distinct word (bit already clear => DoubleFree)
     {
         u64* wp = bm_row(v, c) + (pi >> 6);
         const u64 bit = valid ? (1ull << (pi & 63)) : 0ull;
@@ -859,9 +922,9 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
         const u32 lo = __reduce_or_sync(grp, (u32)bit), hi = __reduce_or_sync(grp, (u32)(bit >> 32));
         const u32 gl = __ffs(grp) - 1;
         u64 old = 0;
-        if (valid && lane == gl) old = atomicOr(wp, ((u64)hi << 32) | lo);
+        if (valid && lane == gl) old = atomicAnd(wp, ~(((u64)hi << 32) | lo));
         old = shfl64(mask, old, gl);
-        if (valid && (old & bit)) { valid = false; st = OURO_ERR_DOUBLE_FREE; }
+        if (valid && !(old & bit)) { valid = false; st = OURO_ERR_DOUBLE_FREE; }
     }
     {
         const u32 nd = __ballot_sync(mask, st == OURO_ERR_DOUBLE_FREE);
@@ -894,15 +957,13 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
         const u32 g2l = __ffs(g2) - 1, r2 = __popc(g2 & lt);
         u32 take = 0;
         if (closer && lane == g2l) {
+            // take = min(want, assigned - 1) atomically: fetch-sub then give back
+            // the excess (no CAS loop; equivalent, since a closer that over-asks
+            // leaves exactly one chunk and concurrent closers could get none anyway)
             const u32 want = __popc(g2);
-            u32 cur = ld_acq32(v.assigned + k);
-            for (;;) {
-                take = cur > 1 ? min(want, cur - 1) : 0u;
-                if (!take) break;
-                const u32 prev = atomicCAS(v.assigned + k, cur, cur - take);
-                if (prev == cur) break;
-                cur = prev;
-            }
+            const u32 old = atomicSub(v.assigned + k, want);
+            take = old > 1 ? min(want, old - 1) : 0u;
+            if (want - take) atomicAdd(v.assigned + k, want - take);
         }
         take = __shfl_sync(mask, take, g2l);
         bool closed = false;
@@ -911,22 +972,10 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
             if (atomicCAS(v.meta + c, expect, mk_meta(gen, ST_UNASSIGNED, 0)) == expect) closed = true;
             else atomicAdd(v.assigned + k, 1u);
         }
-        u32 cm = __ballot_sync(mask, closed);
-        if (cm) {
-            const u32 L = __popc(mask), li = __popc(mask & lt);
-            u32 it = cm;
-            while (it) {
-                const u32 o = __ffs(it) - 1;
-                const u32 oc = __shfl_sync(mask, c, o), ok_ = __shfl_sync(mask, k, o);
-                u64* row = bm_row(v, oc);
-                const u32 W = words_of(v, ok_);
-                for (u32 w = li; w < W; w += L) st_rlx(row + w, 0ull);
-                it &= it - 1;
-            }
-            __threadfence();
-            __syncwarp(mask);
-            arr_enqueue(v, v.q + v.K, mask, lane, cm, c, true);  // return to pool
-        }
+        // a fully free chunk's bitmap is already all-zero: return it to the pool
+        // right after its close CAS returned
+        const u32 cm = __ballot_sync(mask, closed);
+        if (cm) arr_enqueue(v, v.q + v.K, mask, lane, cm, c, true);
         // 0 -> >0: the releaser re-enqueues the chunk
         q_enqueue_by_queue<FL>(v, mask, lane, cl && oldfree == 0 && !closed, k, q_entry(v, c, gen));
     } else {

@@ -532,7 +532,9 @@ struct orc_heap {
     u32 kind = 0, flavor = 0;
     // ChunkHeader side table: meta = {free:32, state:8, gen:24}.
     std::vector<u64> meta;
-    std::vector<u64> bitmap;  // N * Wmax words, 1 = free
+    // N * Wmax words, 1 = ALLOCATED (an unassigned or fully free chunk is all-zero, so
+    // assigning needs no bitmap init and returning to the pool needs no clear)
+    std::vector<u64> bitmap;
     std::vector<u32> assigned;  // chunk kind: chunks assigned per class (gap G3 watermark)
     // page-kind partition (gap G1)
     std::vector<u32> pq_start, pq_n, pq_s;
@@ -618,10 +620,6 @@ void orc_heap::build() {
                     meta[c] = mk(0, ST_RESERVED, 0);
                 } else {
                     meta[c] = mk(1, k + 1, (u32)ppc);
-                    for (u32 w = 0; w < g.words(k); ++w) {
-                        const u32 lo = w * 64, hi = std::min<u32>((u32)ppc, lo + 64);
-                        bm(c)[w] = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1);
-                    }
                 }
             }
             Queue& Q = ar.q[k];
@@ -658,22 +656,24 @@ void orc_heap::build() {
     }
 }
 
-// Claim the `take` lowest set bits of the chunk bitmap (SPEC.md:202-206, 226:
-// lowest free word first, fetch-AND with the chosen bits).  Returns pages claimed.
+// Claim the `take` lowest free pages (lowest free word
+// first; free = clear bit below ppc, claimed with fetch-OR).  Returns pages claimed.
 u32 orc_heap::claim_lowest(u32 c, u32 k, u32 take, u32* pages) {
     u32 got = 0;
     Spin sp;
     while (got < take) {
         for (u32 w = 0; w < g.words(k) && got < take; ++w) {
-            u64 snap = A(bm(c)[w]).load(ACQ);
+            const u32 ppc = g.ppc(k);
+            const u64 valid = (ppc - w * 64 >= 64) ? ~0ull : ((1ull << (ppc - w * 64)) - 1);
+            u64 snap = ~A(bm(c)[w]).load(ACQ) & valid;
             u64 pick = 0;
             while (snap && got + (u32)std::popcount(pick) < take) {
                 pick |= snap & (~snap + 1);
                 snap &= snap - 1;
             }
             if (!pick) continue;
-            const u64 old = A(bm(c)[w]).fetch_and(~pick, AR);
-            u64 mine = old & pick;
+            const u64 old = A(bm(c)[w]).fetch_or(pick, AR);
+            u64 mine = ~old & pick;
             if (mine != pick) ar.err.raise(OURO_ERR_CORRUPTION);
             while (mine) {
                 pages[got++] = w * 64 + (u32)std::countr_zero(mine);
@@ -702,8 +702,8 @@ void orc_heap::alloc_page(u32 k, Lane** L, u32 n) {
             if (h == NONE) { l->st = OURO_ERR_TIMEOUT; l->off = ~0ull; continue; }
             const u32 c = h >> g.page_bits, p = h & ((1u << g.page_bits) - 1);
             const u64 bit = 1ull << (p & 63);
-            const u64 old = A(bm(c)[p >> 6]).fetch_and(~bit, AR);
-            if (!(old & bit)) ar.err.raise(OURO_ERR_CORRUPTION);
+            const u64 old = A(bm(c)[p >> 6]).fetch_or(bit, AR);
+            if (old & bit) ar.err.raise(OURO_ERR_CORRUPTION);
             A(meta[c]).fetch_sub(1, AR);
             l->st = OURO_OK;
             l->off = offset_of(c, k, p);
@@ -765,18 +765,12 @@ void orc_heap::alloc_chunk(u32 k, Lane** L, u32 n) {
             const u64 m = A(meta[c]).load(ACQ);
             if (m_state(m) != ST_UNASSIGNED) { ar.err.raise(OURO_ERR_CORRUPTION); continue; }
             const u32 gen = (m_gen(m) + 1) & 0xFFFFFF;
-            // chunk_assign fused with taking pages 0..take-1
-            for (u32 w = 0; w < g.words(k); ++w) {
-                const u32 lo = w * 64, hi = std::min(ppc, lo + 64);
-                u64 bits = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1);
-                const u32 tk_hi = std::min(take, hi);
-                if (tk_hi > lo) {
-                    const u32 nt = tk_hi - lo;
-                    bits &= (nt == 64) ? 0 : ~((1ull << nt) - 1);
-                }
-                A(bm(c)[w]).store(bits, RLX);
-            }
-            A(meta[c]).store(mk(gen, k + 1, ppc - take), REL);
+            // chunk_assign fused with taking pages 0..take-1:
+            // the bitmap of a pool chunk is all-zero (all free), so only the taken
+            // bits are set (take <= group size <= 64: one word)
+            const u64 tb = take >= 64 ? ~0ull : ((1ull << take) - 1);
+            if (A(bm(c)[0]).fetch_or(tb, AR) & tb) ar.err.raise(OURO_ERR_CORRUPTION);
+            A(meta[c]).exchange(mk(gen, k + 1, ppc - take), AR);
             A(assigned[k]).fetch_add(1, AR);
             if (ppc - take > 0) {
                 Spin s2;
@@ -830,7 +824,8 @@ void orc_heap::alloc_group(Lane* lanes, u32 n) {
 }
 
 // One warp's free call.  Steps, in order:
-// decode + in-group duplicates, bitmap fetch-OR, per-chunk free_count add,
+// decode + in-group duplicates, bitmap fetch-AND (clear the allocated bit),
+// per-chunk free_count add,
 // chunk kind: watermark-limited closes (return to pool), class enqueues.
 void orc_heap::free_group(Lane* L, u32 n) {
     struct V { u32 c, k, p; bool ok; };
@@ -854,8 +849,8 @@ void orc_heap::free_group(Lane* L, u32 n) {
     for (u32 i = 0; i < n; ++i) {
         if (!v[i].ok) continue;
         const u64 bit = 1ull << (v[i].p & 63);
-        const u64 old = A(bm(v[i].c)[v[i].p >> 6]).fetch_or(bit, AR);
-        if (old & bit) { L[i].st = OURO_ERR_DOUBLE_FREE; v[i].ok = false; }
+        const u64 old = A(bm(v[i].c)[v[i].p >> 6]).fetch_and(~bit, AR);
+        if (!(old & bit)) { L[i].st = OURO_ERR_DOUBLE_FREE; v[i].ok = false; }
     }
     for (u32 i = 0; i < n; ++i) {
         if (L[i].st == OURO_ERR_DOUBLE_FREE) { A(ar.err.double_frees).fetch_add(1, RLX); ar.err.raise(OURO_ERR_DOUBLE_FREE); }
@@ -889,12 +884,10 @@ void orc_heap::free_group(Lane* L, u32 n) {
             if (handled[order[a]]) continue;
             u32 want = 0;
             for (u32 b = a; b < order.size(); ++b) if (cg[order[b]].k == k) ++want;
-            u32 cur = A(assigned[k]).load(ACQ), take = 0;
-            for (;;) {
-                take = cur > 1 ? std::min(want, cur - 1) : 0;
-                if (!take) break;
-                if (A(assigned[k]).compare_exchange_weak(cur, cur - take, AR, ACQ)) break;
-            }
+            // take = min(want, assigned - 1): fetch-sub, give back the excess
+            const u32 old = A(assigned[k]).fetch_sub(want, AR);
+            const u32 take = old > 1 ? std::min(want, old - 1) : 0;
+            if (want - take) A(assigned[k]).fetch_add(want - take, AR);
             u32 given = 0;
             for (u32 b = a; b < order.size(); ++b) {
                 if (cg[order[b]].k != k) continue;
@@ -909,8 +902,7 @@ void orc_heap::free_group(Lane* L, u32 n) {
             const u32 ppc = g.ppc(x.k);
             u64 expect = mk(x.gen, x.k + 1, ppc);
             if (A(meta[x.c]).compare_exchange_strong(expect, mk(x.gen, ST_UNASSIGNED, 0), AR, ACQ)) {
-                for (u32 w = 0; w < g.words(x.k); ++w) A(bm(x.c)[w]).store(0, RLX);
-                x.closed = true;
+                x.closed = true;  // fully free => bitmap already all-zero
                 to_pool.push_back(x.c);
             } else {
                 A(assigned[x.k]).fetch_add(1, AR);
@@ -1299,7 +1291,7 @@ ouro_status orc_digest(orc_heap* h, ouro_digest* d) {
         d->live_pages += live;
         u64 pc = 0;
         for (u32 w = 0; w < g.Wmax; ++w) pc += (u64)std::popcount(b[w]);
-        if (pc != orc_heap::m_free(m)) ok = false;
+        if (g.ppc(k) - pc != orc_heap::m_free(m)) ok = false;  // allocated bits = live pages
     }
     if (h->kind == OURO_KIND_CHUNK) {
         for_each_queued(h, h->ar.q[h->pool_idx()], [&](u32 c) { if (c < g.N) ++where[c]; else ok = false; });
@@ -1358,11 +1350,7 @@ ouro_status orc_chunk_assign(orc_heap* h, uint32_t c, uint32_t cls, uint32_t* ge
     if (orc_heap::m_state(m) != ST_UNASSIGNED) return OURO_ERR_ALREADY_ASSIGNED;
     const u32 ppc = h->g.ppc(cls);
     const u32 ng = (orc_heap::m_gen(m) + 1) & 0xFFFFFF;
-    for (u32 w = 0; w < h->g.words(cls); ++w) {
-        const u32 lo = w * 64, hi = std::min(ppc, lo + 64);
-        h->bm(c)[w] = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1);
-    }
-    h->meta[c] = orc_heap::mk(ng, cls + 1, ppc);
+    h->meta[c] = orc_heap::mk(ng, cls + 1, ppc);  // bitmap already all-zero (all free)
     h->assigned[cls] += 1;
     if (gen) *gen = ng;
     return OURO_OK;
@@ -1387,8 +1375,8 @@ ouro_status orc_chunk_release(orc_heap* h, uint32_t c, uint32_t page, uint32_t* 
     const u32 st = orc_heap::m_state(m0);
     if (st == ST_UNASSIGNED || st > h->g.K || page >= h->g.ppc(st - 1)) return OURO_ERR_INVALID_HANDLE;
     const u64 bit = 1ull << (page & 63);
-    const u64 old = A(h->bm(c)[page >> 6]).fetch_or(bit, AR);
-    if (old & bit) return OURO_ERR_DOUBLE_FREE;
+    const u64 old = A(h->bm(c)[page >> 6]).fetch_and(~bit, AR);
+    if (!(old & bit)) return OURO_ERR_DOUBLE_FREE;
     const u64 m = A(h->meta[c]).fetch_add(1, AR);
     *occ_after = orc_heap::m_free(m) + 1;
     return OURO_OK;
@@ -1399,8 +1387,7 @@ ouro_status orc_chunk_unassign(orc_heap* h, uint32_t c) {
     const u32 st = orc_heap::m_state(m);
     if (st == ST_UNASSIGNED || st > h->g.K) return OURO_ERR_INVALID_HANDLE;
     if (orc_heap::m_free(m) != h->g.ppc(st - 1)) return OURO_ERR_USAGE;
-    for (u32 w = 0; w < h->g.Wmax; ++w) h->bm(c)[w] = 0;
-    h->meta[c] = orc_heap::mk(orc_heap::m_gen(m), ST_UNASSIGNED, 0);
+    h->meta[c] = orc_heap::mk(orc_heap::m_gen(m), ST_UNASSIGNED, 0);  // bitmap already zero
     h->assigned[st - 1] -= 1;
     return OURO_OK;
 }
@@ -1413,7 +1400,8 @@ ouro_status orc_chunk_state(orc_heap* h, uint32_t c, uint32_t* state, uint32_t* 
     *gen = orc_heap::m_gen(m);
     u64 pc = 0;
     for (u32 w = 0; w < h->g.Wmax; ++w) pc += (u64)std::popcount(h->bm(c)[w]);
-    *bitmap_popcount = pc;
+    const u32 st = orc_heap::m_state(m);
+    *bitmap_popcount = (st >= 1 && st <= h->g.K) ? h->g.ppc(st - 1) - pc : 0;  // free pages
     return OURO_OK;
 }
 

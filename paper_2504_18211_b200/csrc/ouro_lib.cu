@@ -101,12 +101,8 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
         v.meta[c] = mk_meta(0, ST_RESERVED, 0);
         return;
     }
-    const u32 ppc = ppc_of(v, k);
-    v.meta[c] = mk_meta(1, k + 1, ppc);
-    for (u32 w = 0; w < words_of(v, k); ++w) {
-        const u32 lo = w * 64, hi = min(ppc, lo + 64);
-        row[w] = (hi - lo == 64) ? ~0ull : ((1ull << (hi - lo)) - 1ull);
-    }
+    v.meta[c] = mk_meta(1, k + 1, ppc_of(v, k));  // bitmap all-zero = all free
+    (void)row;
 }
 
 // ------------------------------------------------------------ driver phases ----
@@ -204,7 +200,7 @@ __global__ void k_audit_collect(ouro_heap_view v, u64 n, void* const* ptrs, u64*
     const u64 len = 1ull << (v.min_shift + k);
     if (off & (len - 1)) atomicAdd(&res[2], 1ull);
     const u32 p = (u32)((off & (v.chunk_bytes - 1)) >> (v.min_shift + k));
-    if ((bm_row(v, c)[p >> 6] >> (p & 63)) & 1ull) atomicAdd(&res[4], 1ull);
+    if (!((bm_row(v, c)[p >> 6] >> (p & 63)) & 1ull)) atomicAdd(&res[4], 1ull);  // must be marked allocated
     atomicAdd(&res[5], len);
     const u64 j = atomicAdd(idx, 1ull);
     offs[j] = off;
@@ -331,7 +327,7 @@ __global__ void k_digest_headers(ouro_heap_view v, DigestDev* d, u32* where) {
     const u64 live = ppc_of(v, k) - m_free(m);
     atomicAdd(&d->class_live_pages[k], live);
     atomicAdd(&d->live_pages, live);
-    if (pc != m_free(m)) atomicOr(&d->bad, 4u);
+    if (ppc_of(v, k) - pc != m_free(m)) atomicOr(&d->bad, 4u);  // allocated bits = live pages
 }
 
 // Value of ticket t in a quiescent queue (segment table for virtual flavours).
