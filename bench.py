@@ -194,6 +194,21 @@ def cpu_baseline(cfgname):
 
 
 # ------------------------------------------------------------------ GPU ----
+def job_totals(tot_ms, tot_ok, world, device):
+    """Whole-job totals for weak scaling: time = MAX over ranks of the device
+    time, work = SUM over ranks of successful pairs (independent heaps, no
+    collective on the data path; this reduction is bookkeeping only)."""
+    if world <= 1:
+        return float(tot_ms), float(tot_ok)
+    import torch
+    import torch.distributed as dist
+    tmax = torch.tensor([float(tot_ms)], dtype=torch.float64, device=device)
+    tsum = torch.tensor([float(tot_ok)], dtype=torch.float64, device=device)
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    return float(tmax[0]), float(tsum[0])
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -276,15 +291,7 @@ def main():
     err = heap.last_error()
     tot_ms = sum(sum(p["alloc_ms"]) + sum(p["free_ms"]) for p in per.values())
     tot_ok = sum(sum(p["ok"]) for p in per.values())
-    t = torch.tensor([tot_ms, float(tot_ok)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        tmax = t.clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t.clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_job, ok_job = float(tmax[0]), float(tsum[1])
-    else:
-        ms_job, ok_job = tot_ms, float(tot_ok)
+    ms_job, ok_job = job_totals(tot_ms, tot_ok, world, "cuda")
     value = ok_job / (ms_job / 1e3)
 
     # ---------------- e2e through the public C-ABI with host buffers ----------------

@@ -705,7 +705,8 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     while (todo) {
         const u32 rank = __popc(todo & lt);
         u32 h = NONE;
-        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h, attempt > 0, attempt > 0);
+        // retry tries follow a poll that saw the queue non-empty: straight to the RMW
+        const u32 got = q_dequeue<FL>(v, k, mask, lane, todo, 0, &h, false, false);
         const bool mine = ((todo >> lane) & 1u) && rank < got;
         bool ok = mine && h != NONE;
         u32 c = 0, p = 0;
@@ -739,13 +740,29 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         }
         todo &= ~__ballot_sync(mask, mine);
         if (!todo) break;
-        retries += (u64)__popc(todo);
-        if (++attempt >= v.max_retries) {
-            if (lane == gl0) atomicAdd(&v.ctr[v.K + k], (u64)__popc(todo));
+        // Failed try.  Further failed rounds run on the leader alone: backoff,
+        // then the block-combined poll; the full reservation is retried only
+        // when a poll says the queue is non-empty.  Round accounting is the
+        // oracle's (one failed try per round, OOM after max_retries).
+        const u32 leader = __ffs(todo) - 1, rem = __popc(todo);
+        u32 a = attempt, oom = 0;
+        if (lane == leader) {
+            for (;;) {
+                ++a;
+                if (a >= v.max_retries) { oom = 1; break; }
+                backoff(v, a);
+                if (!observed_empty(v.q + k, 0)) break;
+            }
+        }
+        a = __shfl_sync(mask, a, leader);
+        oom = __shfl_sync(mask, oom, leader);
+        retries += (u64)rem * (a - attempt);
+        attempt = a;
+        if (oom) {
+            if (lane == gl0) atomicAdd(&v.ctr[v.K + k], (u64)rem);
             if ((todo >> lane) & 1u) *st = OURO_ERR_OOM;
             break;
         }
-        backoff(v, attempt);
     }
     if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);  // one update per call, not per round
 }
@@ -835,13 +852,25 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             todo &= ~__ballot_sync(mask, intodo && rank < take);
             continue;
         }
-        retries += n;
-        if (++attempt >= v.max_retries) {
+        // both empty: failed rounds on the leader alone until a poll sees work
+        u32 a = attempt, oom = 0;
+        if (lane == leader) {
+            for (;;) {
+                ++a;
+                if (a >= v.max_retries) { oom = 1; break; }
+                backoff(v, a);
+                if (!observed_empty(v.q + k, 0) || !observed_empty(v.q + pool, v.floor_F)) break;
+            }
+        }
+        a = __shfl_sync(mask, a, leader);
+        oom = __shfl_sync(mask, oom, leader);
+        retries += (u64)n * (a - attempt);
+        attempt = a;
+        if (oom) {
             if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)n);
             if (intodo) *st = OURO_ERR_OOM;
             break;
         }
-        backoff(v, attempt);
     }
     if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);
 }
