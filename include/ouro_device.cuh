@@ -162,14 +162,15 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 // ------------------------------------------------------- count / tickets ----
 // Per-block poll combining for retry rounds.  Retrying warps (OOM storms:
 // ~10^6 lanes x max_retries rounds) would otherwise all poll the same count
-// word, and same-address loads serialise in one L2 slice.  Within a block, the
-// first warp to need a fresh observation of a queue becomes the poller (CAS on
-// a shared-memory entry marked in-flight), the others wait (bounded) for its
-// result.  The result is at most kPollWindow old, i.e. equivalent to having
-// polled that much earlier; a non-empty result still goes through the
-// authoritative reservation RMW.  Entry: [63:8] time/256 ns, [7:2] queue tag,
-// [1] in flight, [0] empty.
-constexpr u64 kPollWindow = 8;  // x 256 ns
+// word, and same-address loads serialise in one L2 slice.  Within a block the
+// first warp that needs a fresh observation of a queue becomes the poller (CAS
+// marks the entry in flight); while a refresh is in flight the other warps
+// reuse the previous completed observation (at most 4 windows old) instead of
+// waiting for L2.  Every observation is therefore at most ~33 us old --
+// equivalent to having polled that much earlier -- and a non-empty answer
+// still goes through the authoritative reservation RMW.
+// Entry: [63:8] time/256 ns, [7:3] queue tag, [2] no result yet, [1] in flight, [0] empty.
+constexpr u64 kPollWindow = 32;  // x 256 ns = 8.2 us
 __device__ __forceinline__ u64 gtime256() {
     u64 t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -179,20 +180,25 @@ __device__ __forceinline__ u64* poll_cache() {
     __shared__ u64 cache[8];
     return cache;
 }
-// true: the queue was observed (count - floor <= 0) within the window
+// true: the queue was observed (count - floor <= 0) recently
 __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
-    const u64 tag = (((u64)Q >> 10) ^ ((u64)Q >> 16)) & 63u;
+    const u64 tag = (((u64)Q >> 10) ^ ((u64)Q >> 15)) & 31u;
     u64* slot = poll_cache() + (tag & 7);
-    for (int spins = 0; spins < 64; ++spins) {
+    for (int spins = 0; spins < 256; ++spins) {
         const u64 now = gtime256();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
-        const bool fresh = ((e >> 2) & 63u) == tag && now - (e >> 8) < kPollWindow;
-        if (fresh && !(e & 2u)) return (e & 1u) != 0;
-        if (fresh) { __nanosleep(32); continue; }  // another warp's poll in flight
-        const u64 mine = (now << 8) | (tag << 2) | 2u;
+        const bool match = ((e >> 3) & 31u) == tag;
+        // signed: an entry written after we read the clock is fresh, not stale
+        const i64 age = (i64)(now - (e >> 8));
+        if (match && !(e & 4u)) {
+            if (!(e & 2u) && age < (i64)kPollWindow) return (e & 1u) != 0;     // fresh
+            if ((e & 2u) && age < 4 * (i64)kPollWindow) return (e & 1u) != 0;  // being refreshed: reuse
+        }
+        if (match && (e & 6u) == 6u && age < 4 * (i64)kPollWindow) { __nanosleep(32); continue; }
+        const u64 mine = (match && !(e & 4u)) ? (e | 2u) : ((now << 8) | (tag << 3) | 6u);
         if (atomicCAS(slot, e, mine) != e) continue;
         const bool empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
-        atomicExch(slot, (gtime256() << 8) | (tag << 2) | (empty ? 1u : 0u));
+        atomicExch(slot, (gtime256() << 8) | (tag << 3) | (empty ? 1u : 0u));
         return empty;
     }
     return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
@@ -907,6 +913,7 @@ template <int KIND, int FL>
 __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32 mask_hint = 0) {
     const u32 mask = mask_hint ? mask_hint : __activemask();
     if (mask_hint) __syncwarp(mask);
+    if (!__ballot_sync(mask, ptr != nullptr)) return OURO_OK;  // free(NULL) for the whole group: no-op
     const u32 lane = lane_id();
     const u32 lt = lanemask_lt();
     int st = OURO_OK;
