@@ -180,10 +180,10 @@ __device__ __forceinline__ u64* poll_cache() {
     __shared__ u64 cache[8];
     return cache;
 }
-// true: the queue was observed (count - floor <= 0) recently
-__device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
-    const u64 tag = (((u64)Q >> 10) ^ ((u64)Q >> 15)) & 31u;
-    u64* slot = poll_cache() + (tag & 7);
+__device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) { return (((u64)Q >> 10) ^ ((u64)Q >> 15)) & 31u; }
+
+// Slow path: become the poller, or wait for / reuse an in-flight poll.
+__device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot) {
     for (int spins = 0; spins < 256; ++spins) {
         const u64 now = gtime256();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
@@ -204,10 +204,39 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
     return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
 }
 
+// true: the queue was observed (count - floor <= 0) recently.  Fast path (a
+// fresh completed entry, or one being refreshed): one LDS, one clock read.
+__device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
+    const u64 tag = poll_tag(Q);
+    u64* slot = poll_cache() + (tag & 7);
+    const u64 e = *reinterpret_cast<volatile u64*>(slot);
+    const i64 age = (i64)(gtime256() - (e >> 8));
+    const u64 d = (e ^ (tag << 3)) & 0xFCu;  // 0: match, completed, idle; 2: match, completed, refreshing
+    if ((d == 0 && age < (i64)kPollWindow) || (d == 2 && age < 4 * (i64)kPollWindow)) return (e & 1u) != 0;
+    return observed_empty_slow(Q, floor, tag, slot);
+}
+
+// Did this block recently see the queue empty?  (hint only: it just turns the
+// first try's RMW into load-then-RMW, which reserves exactly the same.)
+__device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
+    const u64 tag = poll_tag(Q);
+    const u64 e = *reinterpret_cast<volatile u64*>(poll_cache() + (tag & 7));
+    return ((e ^ (tag << 3)) & 0xFDu) == 1u && (i64)(gtime256() - (e >> 8)) < 4 * (i64)kPollWindow;
+}
+__device__ __forceinline__ void note_empty(const ouro_queue_dev* Q) {
+    const u64 tag = poll_tag(Q);
+    u64* slot = poll_cache() + (tag & 7);
+    const u64 e = *reinterpret_cast<volatile u64*>(slot);
+    if ((e & 2u) && ((e >> 3) & 31u) == tag) return;  // a poll is in flight: leave it
+    atomicCAS(slot, e, (gtime256() << 8) | (tag << 3) | 1u);
+}
+
 // Count reservation (broker-queue style).
 // `precheck`: read the count first and skip the RMW when it is already empty
 // (retries and chunk-queue probes); the reservation result is the same either way.
 // `combine`: take the pre-check from the block's poll combiner (retry rounds).
+// Without precheck the first try goes straight to the RMW unless this block saw
+// the queue empty lately (then load first: an OOM storm costs loads, not RMW pairs).
 __device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, bool precheck = true,
                                            bool combine = false) {
     if (precheck) {
@@ -216,11 +245,16 @@ __device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, 
         } else if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
             return 0;
         }
+    } else if (hint_empty(Q) && (i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
+        return 0;
     }
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
-    if (got < n) atomicAdd((u64*)&Q->count, (u64)(n - got));
+    if (got < n) {
+        atomicAdd((u64*)&Q->count, (u64)(n - got));
+        note_empty(Q);
+    }
     return got;
 }
 __device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
