@@ -44,7 +44,15 @@ CONFIGS = {
     "cq1g": ("chunk allocator (CQ), Array queues, 1 GiB heap, 1M threads, 16 B-8 KiB", 1, 0, 1 << 30, 1 << 20, SWEEP[2:]),
     "pq16g4m": ("configs[4] per GPU: PQ, 16 GiB heap, 4M threads, 16 B-1 KiB", 0, 0, 16 << 30, 1 << 22,
                 [16, 32, 64, 128, 256, 512, 1000, 1024]),
+    "cq16g4m": ("configs[4] per GPU: CQ, 16 GiB heap, 4M threads, 16 B-1 KiB", 1, 0, 16 << 30, 1 << 22,
+                [16, 32, 64, 128, 256, 512, 1000, 1024]),
+    # configs[3]: mixed churn; a step = 10 rounds, sizes 8 B-4 KiB drawn per (thread, round)
+    "churn": ("configs[3]: mixed churn, CQ, 16 GiB heap, 4M threads, sizes 8 B-4 KiB, 10 rounds per step",
+              1, 0, 16 << 30, 1 << 22, None),
+    "churn-pq": ("configs[3]: mixed churn, PQ, 16 GiB heap, 4M threads, sizes 8 B-4 KiB, 10 rounds per step",
+                 0, 0, 16 << 30, 1 << 22, None),
 }
+CHURN_ROUNDS_PER_STEP = 10
 HEADLINE_RANGE = (16, 1024)  # BASELINE target band
 
 
@@ -134,6 +142,29 @@ def run_reference(args, cfgname):
     cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
     L = oracle()
     oh = OHeap(cfg)
+    if sizes is None:  # churn: ops = mallocs + frees per second
+        from paper_2504_18211_b200._abi import ChurnResult
+        slots = (C.c_uint64 * sample)(*([2 ** 64 - 1] * sample))
+        tot_ops, tot_s, r0 = 0, 0.0, 0
+        for step in range(args.warmup + args.steps):
+            res, ms = ChurnResult(), C.c_double()
+            assert L.orc_churn(oh.h, sample, r0, CHURN_ROUNDS_PER_STEP, 1, threads, slots, C.byref(res),
+                               C.byref(ms)) == 0
+            r0 += CHURN_ROUNDS_PER_STEP
+            if step >= args.warmup:
+                tot_ops += res.mallocs_ok + res.mallocs_failed + res.frees
+                tot_s += ms.value / 1e3
+        value = tot_ops / tot_s
+        print(json.dumps({
+            "metric": "churn malloc+free ops/s", "impl": "reference", "value": value, "unit": "ops/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * tot_s / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/u64", "data": "synthetic",
+            "config": {"workload": desc, "sample_threads": sample},
+            "cpu_baseline": {"value": value, "unit": "ops/s", "cores": threads, "kind": "port",
+                             "sample": f"{sample} slots x {CHURN_ROUNDS_PER_STEP} rounds per step"},
+            "e2e": {"value": value, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
 
     def one_step():
         ok = 0
@@ -226,6 +257,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     desc, kind, flavor, heap_bytes, n, sizes = CONFIGS[args.config]
+    if sizes is None:
+        return run_churn(args, world, rank, local, desc, kind, flavor, heap_bytes, n)
     if args.sizes:
         sizes = [int(x) for x in args.sizes.split(",")]
     hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
@@ -378,6 +411,64 @@ def main():
         "cpu_baseline": cpu,
     }
     print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_churn(args, world, rank, local, desc, kind, flavor, heap_bytes, n):
+    """BASELINE configs[3]: 4M threads, interleaved alloc/free rounds (one kernel
+    per round: each thread frees its slot on odd hash, else mallocs 8 B-4 KiB and
+    stamps it; occupied even-hash slots check their stamp).  ops = mallocs
+    (successful or not) + frees; fragmentation = live bytes / bytes of assigned
+    chunks; reuse = mallocs served from pages handed out before."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_18211_b200 as ob
+    hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
+    heap = ob.Heap(hc, local)
+    slots = torch.zeros(n, dtype=torch.int64, device="cuda")
+    res = torch.zeros(5, dtype=torch.int64, device="cuda")
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    r0 = 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            heap.launch_churn(n, r0, CHURN_ROUNDS_PER_STEP, 1, slots, res)
+            r0 += CHURN_ROUNDS_PER_STEP
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        res.zero_()
+        ms = 0.0
+        for _ in range(args.steps):
+            ev[0].record()
+            heap.launch_churn(n, r0, CHURN_ROUNDS_PER_STEP, 1, slots, res)
+            ev[1].record()
+            ev[1].synchronize()
+            ms += ev[0].elapsed_time(ev[1])
+            r0 += CHURN_ROUNDS_PER_STEP
+    ok, failed, frees, reused, bad = [int(x) for x in res]
+    ops = ok + failed + frees
+    ms_job, ops_job = job_totals(ms, ops, world, "cuda")
+    a = heap.audit(n, slots)
+    st = heap.stats()
+    assigned = sum(st.cls[k].chunks for k in range(st.num_classes))
+    frag = a.bytes / (assigned * hc.chunk_bytes) if assigned else None
+    if rank == 0:
+        print(json.dumps({
+            "metric": "churn malloc+free ops/s", "value": ops_job / (ms_job / 1e3), "unit": "ops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_job / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
+            "data": "synthetic",
+            "config": {"workload": desc, "variant": ob.variant_name(hc.variant), "threads": n,
+                       "rounds_timed": args.steps * CHURN_ROUNDS_PER_STEP,
+                       "mallocs_ok": ok, "mallocs_failed": failed, "frees": frees,
+                       "reuse_fraction": reused / ok if ok else None, "stamp_check_failures": bad,
+                       "live_allocations": a.live, "live_bytes": a.bytes, "assigned_chunks": assigned,
+                       "fragmentation_live_over_assigned": frag,
+                       "audit_overlaps": a.overlaps, "sticky_error": heap.last_error()[0]},
+            "gpu_launches": args.steps * CHURN_ROUNDS_PER_STEP, "clocks": clk.summary()}))
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
