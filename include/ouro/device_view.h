@@ -49,7 +49,13 @@ typedef struct ouro_queue_dev {
     uint32_t* dcnt;
     ouro_u64 seg_live;                 /* stats */
     ouro_u64 seg_hwm;
-    uint8_t pad5[OURO_HOT_STRIDE - 80];
+    /* VirtualList lookup accelerator: links {seq:32|chunk:32} of the
+     * OURO_VL_RECENT most recently created segments at [seq % OURO_VL_RECENT].
+     * The list itself stays the source of truth; an entry is used only when its
+     * seq matches (a segment cannot retire while a caller still needs it). */
+#define OURO_VL_RECENT 256
+    ouro_u64 vl_recent[OURO_VL_RECENT];
+    uint8_t pad5[3 * OURO_HOT_STRIDE - 80 - 8 * OURO_VL_RECENT];
 } ouro_queue_dev;
 
 /* Counter indices in ctr[] (after 2*K per-class retries/ooms). */

@@ -59,6 +59,15 @@ __device__ __forceinline__ u64 ld_acq(const u64* p) {
 __device__ __forceinline__ u32 ld_acq32(const u32* p) {
     u32 r; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory"); return r;
 }
+__device__ __forceinline__ u32 ld_rlx32(const u32* p) {
+    u32 r; asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory"); return r;
+}
+// Reads of directory entries / segment links / segment headers use ld_rlx,
+// not ld.acquire: every such value is the address of the next access (the
+// hardware cannot issue that access before the load returns), and publishers
+// fence before their release store, so an acquire would only add its
+// CCTL.IVALL (an L1 invalidate per lookup -- measured as the dominant stall of
+// the virtual-list free path).
 __device__ __forceinline__ void ld_rlx_v2(const u64* p, u64& a, u64& b) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
 }
@@ -183,7 +192,7 @@ __device__ __forceinline__ u64* poll_cache() {
 __device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) { return (((u64)Q >> 10) ^ ((u64)Q >> 15)) & 31u; }
 
 // Slow path: become the poller, or wait for / reuse an in-flight poll.
-__device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot) {
+static __device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot) {
     for (int spins = 0; spins < 256; ++spins) {
         const u64 now = gtime256();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
@@ -382,7 +391,7 @@ __device__ __forceinline__ bool va_find(const ouro_heap_view& v, ouro_queue_dev*
     u64* e = Q->dir + (s % Q->D);
     Spin sp;
     for (;;) {
-        const u64 x = ld_acq(e);
+        const u64 x = ld_rlx(e);
         if ((u32)(x >> 32) == (u32)s && (u32)x != NONE) { *c = (u32)x; return true; }
         if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
     }
@@ -394,7 +403,7 @@ __device__ __forceinline__ bool va_create(const ouro_heap_view& v, ouro_queue_de
     if (lane == who) {
         const u64 want = ((u64)(u32)s << 32) | NONE;
         Spin sp;
-        while (ld_acq(e) != want)
+        while (ld_rlx(e) != want)
             if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); ok = 0; break; }
     }
     ok = __shfl_sync(mask, ok, who);
@@ -419,19 +428,36 @@ __device__ __forceinline__ u32* vl_counter(const ouro_heap_view& v, u32 c) {
     return reinterpret_cast<u32*>(chunk_words(v, c) + 1);
 }
 
-__device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_dev* Q, u64 s, u32* out) {
+// Find the chunk of segment s.  First the ring of recently created segments
+// (vl_recent, written by each creator right after it links its segment).
+// from_tail (enqueuers, segment creators): the target is the newest segment or
+// one being created now, so a ring slot still holding an older segment means
+// "not created yet": wait on that slot (waiters of different segments poll
+// different lines, not the one tail word the creators update).  Only a target
+// older than the ring, or a dequeuer's target, is walked from the head; a walk
+// validates every hop against the head so a retired segment is never followed.
+__device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_dev* Q, u64 s, u32* out,
+                                          bool from_tail = false) {
     Spin sp;
     for (;;) {
-        const u64 tl = ld_acq(&Q->vl_tail);
+        const u64 r = ld_rlx(&Q->vl_recent[s % OURO_VL_RECENT]);
+        if (lchk(r) != NONE && lseq(r) == (u32)s) { *out = lchk(r); return true; }
+        if (from_tail && (lchk(r) == NONE || (int)((u32)s - lseq(r)) > 0)) {  // creator of s not done yet
+            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
+            continue;
+        }
+        const u64 tl = ld_rlx(&Q->vl_tail);
         if (lchk(tl) != NONE && lseq(tl) == (u32)s) { *out = lchk(tl); return true; }
-        const u64 h = ld_acq(&Q->vl_head);
+        const u64 h = ld_rlx(&Q->vl_head);
         if (lchk(h) != NONE) {
             u32 i = lseq(h), cur = lchk(h);
             if ((u32)((u32)s - i) >= 0x80000000u) { raise_err(v, OURO_ERR_CORRUPTION); return false; }
             bool ok = true;
             while (i != (u32)s) {
-                const u64 nx = ld_acq(chunk_words(v, cur));
-                if (ld_acq(&Q->vl_head) != h || nx == NONE_LINK) { ok = false; break; }
+                const u64 nx = ld_rlx(chunk_words(v, cur));
+                // the link read is valid iff segment i was not retired before it:
+                // retirement moves the head past i first, so re-check the head's seq
+                if ((int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0 || nx == NONE_LINK) { ok = false; break; }
                 cur = lchk(nx);
                 ++i;
             }
@@ -441,7 +467,7 @@ __device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_de
     }
 }
 __device__ __forceinline__ void vl_tail_max(ouro_queue_dev* Q, u64 l) {
-    u64 cur = ld_acq(&Q->vl_tail);
+    u64 cur = ld_rlx(&Q->vl_tail);
     for (;;) {
         if (lchk(cur) != NONE && (int)(lseq(l) - lseq(cur)) <= 0) return;
         const u64 prev = atomicCAS((u64*)&Q->vl_tail, cur, l);
@@ -458,10 +484,10 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
     for (;;) {
         u32 go = 0, ch = NONE, released = 0;
         if (lane == who) {
-            u64 h = ld_acq(&Q->vl_head);
+            u64 h = ld_rlx(&Q->vl_head);
             ch = lchk(h);
-            if (ch != NONE && ld_acq32(vl_counter(v, ch)) == full) {
-                const u64 nx = ld_acq(chunk_words(v, ch));
+            if (ch != NONE && ld_rlx32(vl_counter(v, ch)) == full) {
+                const u64 nx = ld_rlx(chunk_words(v, ch));
                 if (nx != NONE_LINK) {
                     go = 1;
                     if (atomicCAS((u64*)&Q->vl_head, h, nx) == h) released = 1;
@@ -498,9 +524,11 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
         seg_count(Q, +1);
         if (s == 0) {
             st_rel(&Q->vl_head, mklink(0, c));
+            st_rel(&Q->vl_recent[0], mklink(0, c));
             vl_tail_max(Q, mklink(0, c));
-        } else if (vl_locate(v, Q, s - 1, &p)) {
+        } else if (vl_locate(v, Q, s - 1, &p, true)) {
             st_rel(chunk_words(v, p), mklink(s, c));
+            st_rel(&Q->vl_recent[s % OURO_VL_RECENT], mklink(s, c));  // wakes the waiters of s
             vl_tail_max(Q, mklink(s, c));
         } else {
             ok = 0;
@@ -517,40 +545,43 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
 template <int FL>
 __device__ __forceinline__ u64 seg_slots(const ouro_heap_view& v) { return FL == FL_VA ? v.S_va : v.S_vl; }
 
+// Chunk holding ticket t's segment, located once per distinct segment of the
+// group (VirtualList: one walk per group instead of one per lane; VirtualArray:
+// one directory read, broadcast).  All lanes of `mask` call it.
 template <int FL>
-__device__ __forceinline__ bool q_put(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32 val) {
-    if (FL == FL_ARRAY) return arr_put(v, Q, t, val);
-    u32 c;
-    u64 j;
-    if (FL == FL_VA) {
-        if (!va_find(v, Q, t / v.S_va, &c)) return false;
-        j = t % v.S_va;
-    } else {
-        if (!vl_locate(v, Q, t / v.S_vl, &c)) return false;
-        j = 2 + t % v.S_vl;
+__device__ __forceinline__ u32 group_segment(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
+                                             bool part, u64 t, bool from_tail) {
+    const u64 s = t / seg_slots<FL>(v);
+    const u32 grp = __match_any_sync(mask, part ? s : (~0ull - lane));
+    const u32 gl = __ffs(grp) - 1;
+    u32 c = NONE;
+    if (part && lane == gl) {
+        bool ok = FL == FL_VA ? va_find(v, Q, s, &c) : vl_locate(v, Q, s, &c, from_tail);
+        if (!ok) c = NONE;
     }
-    st_rlx(chunk_words(v, c) + j, ((u64)vtag(t) << 32) | val);
+    return __shfl_sync(mask, c, gl);
+}
+template <int FL>
+__device__ __forceinline__ u64* slot_in(const ouro_heap_view& v, u32 c, u64 t) {
+    return chunk_words(v, c) + (FL == FL_VA ? t % v.S_va : 2 + t % v.S_vl);
+}
+template <int FL>
+__device__ __forceinline__ bool q_put(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32 val, u32 c) {
+    if (FL == FL_ARRAY) return arr_put(v, Q, t, val);
+    if (c == NONE) return false;
+    st_rlx(slot_in<FL>(v, c, t), ((u64)vtag(t) << 32) | val);
     return true;
 }
 template <int FL>
-__device__ __forceinline__ bool q_take(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32* val, u32* segc) {
-    if (FL == FL_ARRAY) { *segc = NONE; return arr_take(v, Q, t, val); }
-    u32 c;
-    u64 j;
-    if (FL == FL_VA) {
-        if (!va_find(v, Q, t / v.S_va, &c)) return false;
-        j = t % v.S_va;
-    } else {
-        if (!vl_locate(v, Q, t / v.S_vl, &c)) return false;
-        j = 2 + t % v.S_vl;
-    }
-    u64* s = chunk_words(v, c) + j;
+__device__ __forceinline__ bool q_take(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32* val, u32 c) {
+    if (FL == FL_ARRAY) return arr_take(v, Q, t, val);
+    if (c == NONE) return false;
+    u64* s = slot_in<FL>(v, c, t);
     Spin sp;
     u64 x;
     while ((u32)((x = ld_rlx(s)) >> 32) != vtag(t))
         if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
     *val = (u32)x;
-    *segc = c;
     return true;
 }
 
@@ -590,7 +621,8 @@ __device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 m
         good = good && r;
         creators &= creators - 1;
     }
-    if (me) good = q_put<FL>(v, Q, t, val) && good;
+    const u32 c = group_segment<FL>(v, Q, mask, lane, me, t, true);
+    if (me) good = q_put<FL>(v, Q, t, val, c) && good;
     return good;
 }
 
@@ -612,10 +644,10 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
     if (!got) return 0;
     const bool me = ((todo >> lane) & 1u) && rank < got;
     const u64 t = t0 + rank;
-    u32 segc = NONE;
+    const u32 segc = group_segment<FL>(v, Q, mask, lane, me, t, false);
     bool okt = false;
     if (me) {
-        okt = q_take<FL>(v, Q, t, val, &segc);
+        okt = q_take<FL>(v, Q, t, val, segc);
         if (!okt) *val = NONE;
     }
     // consumption bookkeeping per segment (one add per distinct segment)
@@ -630,7 +662,7 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
         if (part && lane == gl) {
             if (atomicAdd(Q->dcnt + (s % Q->D), cnt) + cnt == (u32)v.S_va) {
                 retire = 1;
-                rc = (u32)ld_acq(Q->dir + (s % Q->D));
+                rc = (u32)ld_rlx(Q->dir + (s % Q->D));
             }
         }
         const u32 rm = __ballot_sync(mask, retire);

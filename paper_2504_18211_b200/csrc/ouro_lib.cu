@@ -534,6 +534,7 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
     for (auto& q : H->hq) {
         q.count = 0; q.head = 0; q.tail = 0; q.seg_live = 0; q.seg_hwm = 0;
         q.vl_head = q.vl_tail = ((u64)0 << 32) | NONE;
+        for (auto& r : q.vl_recent) r = NONE_LINK;
     }
     auto ring_fill = [&](ouro_queue_dev& q, u64 cap, int mode, u32 first, u32 ppc) -> ouro_status {
         const u64 R = q.ring_mask + 1;
@@ -587,6 +588,8 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
                 CK(cudaGetLastError());
                 q.vl_head = ((u64)0 << 32) | seg0;
                 q.vl_tail = ((u64)(m - 1) << 32) | (seg0 + m - 1);
+                for (u32 i = m > OURO_VL_RECENT ? m - OURO_VL_RECENT : 0; i < m; ++i)
+                    q.vl_recent[i % OURO_VL_RECENT] = ((u64)i << 32) | (seg0 + i);
             }
             // private segment pool: reserve chunks not used by the prefill
             std::vector<u64> ps(P.ring_mask + 1, 0);
