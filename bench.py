@@ -225,6 +225,16 @@ def cpu_baseline(cfgname):
 
 
 # ------------------------------------------------------------------ GPU ----
+def _traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/r1_traffic.json): the 16 B launch, where all threads are served."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            return json.load(f)["per_launch_dram_bytes"]["16"]
+    except Exception:
+        return None
+
+
 def job_totals(tot_ms, tot_ok, world, device):
     """Whole-job totals for weak scaling: time = MAX over ranks of the device
     time, work = SUM over ranks of successful pairs (independent heaps, no
@@ -398,7 +408,7 @@ def main():
         "roofline": {"bound": "l2_atomic", "kernel": dom,
                      "resource": "same-address RMW chain on the class-queue counters (1 per warp group)",
                      "achieved": achieved / 1e9, "peak": p_same / 1e9, "unit": "Gop/s",
-                     "frac": achieved / p_same, "traffic": None,
+                     "frac": achieved / p_same, "traffic": _traffic(),
                      "peak_source": "measured in-run: ouro_atomic_peak mode 2 (same-address atomicAdd, one per warp)",
                      "distinct_address_peak_gops": p_dist / 1e9,
                      "dominant_kernel_share": dom_ms / (a_ms + f_ms)},
