@@ -186,10 +186,15 @@ __device__ __forceinline__ u64 gtime256() {
     return t >> 8;
 }
 __device__ __forceinline__ u64* poll_cache() {
-    __shared__ u64 cache[8];
+    __shared__ u64 cache[16];
     return cache;
 }
-__device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) { return (((u64)Q >> 10) ^ ((u64)Q >> 15)) & 31u; }
+// Queue structs are laid out consecutively, so the struct index is a collision-free
+// slot for up to 16 consecutive queues (the K class queues and the pool at K <= 15).
+__device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) {
+    return ((u64)Q / sizeof(ouro_queue_dev)) & 31u;
+}
+__device__ __forceinline__ u64* poll_slot(u64 tag) { return poll_cache() + (tag & 15); }
 
 // Slow path: become the poller, or wait for / reuse an in-flight poll.
 static __device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot) {
@@ -217,7 +222,7 @@ static __device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 f
 // fresh completed entry, or one being refreshed): one LDS, one clock read.
 __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
     const u64 tag = poll_tag(Q);
-    u64* slot = poll_cache() + (tag & 7);
+    u64* slot = poll_slot(tag);
     const u64 e = *reinterpret_cast<volatile u64*>(slot);
     const i64 age = (i64)(gtime256() - (e >> 8));
     const u64 d = (e ^ (tag << 3)) & 0xFCu;  // 0: match, completed, idle; 2: match, completed, refreshing
@@ -229,12 +234,12 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
 // first try's RMW into load-then-RMW, which reserves exactly the same.)
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
-    const u64 e = *reinterpret_cast<volatile u64*>(poll_cache() + (tag & 7));
+    const u64 e = *reinterpret_cast<volatile u64*>(poll_slot(tag));
     return ((e ^ (tag << 3)) & 0xFDu) == 1u && (i64)(gtime256() - (e >> 8)) < 4 * (i64)kPollWindow;
 }
 __device__ __forceinline__ void note_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
-    u64* slot = poll_cache() + (tag & 7);
+    u64* slot = poll_slot(tag);
     const u64 e = *reinterpret_cast<volatile u64*>(slot);
     if ((e & 2u) && ((e >> 3) & 31u) == tag) return;  // a poll is in flight: leave it
     atomicCAS(slot, e, (gtime256() << 8) | (tag << 3) | 1u);
@@ -853,7 +858,8 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
         const bool intodo = (todo >> lane) & 1u;
         u32 e = NONE;
-        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, true, attempt > 0);
+        // first try: straight to the RMW unless this block saw the queue empty (hinted)
+        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0);
         e = __shfl_sync(mask, e, leader);
         if (got && e != NONE) {
             const u32 c = e & v.cmask;
@@ -888,7 +894,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             continue;
         }
         u32 c = NONE;
-        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, true, attempt > 0);
+        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, attempt > 0, attempt > 0);
         c = __shfl_sync(mask, c, leader);
         if (got && c != NONE) {
             const u32 take = min(n, ppc);

@@ -106,6 +106,8 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 }
 
 // ------------------------------------------------------------ driver phases ----
+// (Forcing 32 registers for 8 blocks/SM was measured slower: the spills cost
+// more than the extra warps gain, profiles/r1_ncu_summary.md.)
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const u32* sizes, void** out) {
     const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
