@@ -117,14 +117,17 @@ struct Spin {
     }
 };
 
-// backoff: FenceRetry = fence + yield (no sleep);
+// backoff: FenceRetry = a fence between retries, no sleep --
+// the SYCL port's substitute for nanosleep.  The SPEC's extra
+// "yield" is for preemptible CPU threads; warps are hardware-scheduled, and
+// nanosleep(0) alone measured ~300 cycles per round (tools/round_cost.cu).
 // SleepRetry = nanosleep(min(base * 2^attempt, cap)).
 // The retry poll is a .relaxed.gpu load of the queue count, served by L2, so it
 // observes every other SM's frees without any fence; a device-scope fence
 // (fence.sc/acq_rel.gpu -> MEMBAR.GPU + ERRBAR + CCTL.IVALL, measured ~2.5 us
 // per round on B200) would only add delay.  The default therefore fences at CTA
-// scope (orders this warp's own accesses) and yields; build with
-// -DOURO_FENCE_SCOPE_GPU=1 for the literal device-wide seq-cst fence.
+// scope (orders this warp's own accesses); build with -DOURO_FENCE_SCOPE_GPU=1
+// for the literal device-wide seq-cst fence.
 #ifndef OURO_FENCE_SCOPE_GPU
 #define OURO_FENCE_SCOPE_GPU 0
 #endif
@@ -139,7 +142,6 @@ __device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
 #else
         asm volatile("fence.sc.cta;" ::: "memory");
 #endif
-        __nanosleep(0);
     }
 }
 
