@@ -3,6 +3,7 @@
 // reference's config type) and a kernel that calls ouro_malloc / ouro_free
 // per thread.  Built by examples/Makefile against ../paper_2504_18211_b200/libouro_b200.so.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ouro/ouro.hpp"
@@ -33,8 +34,10 @@ __global__ void lists(ouro_heap_view h, int len, unsigned long long* bad) {
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
+    // optional: argv[1] = variant name to run alone
     for (auto v : ouro::kAllVariants) {
+        if (argc > 1 && ouro::variant_name(v) != argv[1]) continue;
         ouro::HeapConfig cfg;                     // reference defaults: 64 MiB, 64 KiB chunks
         cfg.heap_bytes = 256ull << 20;
         cfg.allocator_kind = v.kind;
