@@ -69,6 +69,8 @@ enum {
     OURO_CTR_POOL_DEQ = 6,
     OURO_CTR_N = 8
 };
+/* ctr[] holds OURO_CTR_SHARDS copies of the 2K + OURO_CTR_N counters (by SM). */
+#define OURO_CTR_SHARDS 32
 
 typedef struct ouro_heap_view {
     uint8_t* base;

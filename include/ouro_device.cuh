@@ -49,6 +49,13 @@ constexpr int FL_VL = OURO_FLAVOR_VIRTUAL_LIST;
 // ------------------------------------------------------------ primitives ----
 __device__ __forceinline__ u32 lane_id() { u32 r; asm volatile("mov.u32 %0, %%laneid;" : "=r"(r)); return r; }
 __device__ __forceinline__ u32 lanemask_lt() { u32 r; asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r)); return r; }
+__device__ __forceinline__ u32 sm_id() { u32 r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+// Statistics counters are sharded OURO_CTR_SHARDS ways by SM (the host sums the
+// shards): OOM storms update them once per warp, and unsharded they would be
+// one more same-address RMW chain beside the queue counters.
+__device__ __forceinline__ u64* ctr_at(const ouro_heap_view& v, u32 idx) {
+    return v.ctr + (u64)(sm_id() % OURO_CTR_SHARDS) * (2 * v.K + OURO_CTR_N) + idx;
+}
 
 __device__ __forceinline__ u64 ld_rlx(const u64* p) {
     u64 r; asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory"); return r;
@@ -103,8 +110,8 @@ __device__ __forceinline__ u32 nth_set64(u64 b, u32 x) {
 __device__ __forceinline__ void raise_err(const ouro_heap_view& v, int code) {
     atomicCAS(&v.sticky[0], 0u, (u32)code);
     atomicOr(&v.sticky[1], 1u << code);
-    if (code == OURO_ERR_TIMEOUT) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_TIMEOUT], 1ull);
-    if (code == OURO_ERR_CORRUPTION) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_CORRUPTION], 1ull);
+    if (code == OURO_ERR_TIMEOUT) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_TIMEOUT), 1ull);
+    if (code == OURO_ERR_CORRUPTION) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_CORRUPTION), 1ull);
 }
 
 // Bounded spin: TimeoutError instead of a hung GPU.
@@ -838,12 +845,12 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         retries += (u64)rem * (a - attempt);
         attempt = a;
         if (oom) {
-            if (lane == gl0) atomicAdd(&v.ctr[v.K + k], (u64)rem);
+            if (lane == gl0) atomicAdd(ctr_at(v, v.K + k), (u64)rem);
             if ((todo >> lane) & 1u) *st = OURO_ERR_OOM;
             break;
         }
     }
-    if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);  // one update per call, not per round
+    if (retries && lane == gl0) atomicAdd(ctr_at(v, k), retries);  // one update per call, not per round
 }
 
 // Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).
@@ -877,7 +884,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
                     if (prev == m) { take = t; oldfree = f; break; }
                     m = prev;
                 }
-                if (!take) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_STALE], 1ull);
+                if (!take) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_STALE), 1ull);
             }
             take = __shfl_sync(mask, take, leader);
             oldfree = __shfl_sync(mask, oldfree, leader);
@@ -902,7 +909,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             const u32 take = min(n, ppc);
             u64 m = 0;
             if (lane == leader) {
-                atomicAdd(&v.ctr[2 * v.K + OURO_CTR_POOL_DEQ], 1ull);
+                atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_POOL_DEQ), 1ull);
                 m = ld_rlx(v.meta + c);
             }
             m = shfl64(mask, m, leader);
@@ -947,12 +954,12 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         retries += (u64)n * (a - attempt);
         attempt = a;
         if (oom) {
-            if (lane == leader) atomicAdd(&v.ctr[v.K + k], (u64)n);
+            if (lane == leader) atomicAdd(ctr_at(v, v.K + k), (u64)n);
             if (intodo) *st = OURO_ERR_OOM;
             break;
         }
     }
-    if (retries && lane == gl0) atomicAdd(&v.ctr[k], retries);
+    if (retries && lane == gl0) atomicAdd(ctr_at(v, k), retries);
 }
 
 // malloc for the converged lanes of the calling warp.
@@ -968,7 +975,7 @@ __device__ __forceinline__ void* malloc_impl(const ouro_heap_view& v, u64 bytes,
     void* res = nullptr;
     int st = valid ? OURO_ERR_OOM : OURO_ERR_TOO_LARGE;
     const u32 bad = __ballot_sync(mask, !valid);
-    if (bad && lane == (u32)(__ffs(bad) - 1)) atomicAdd(&v.ctr[2 * v.K + OURO_CTR_BAD_SIZE], (u64)__popc(bad));
+    if (bad && lane == (u32)(__ffs(bad) - 1)) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_BAD_SIZE), (u64)__popc(bad));
     u32 pending = __ballot_sync(mask, valid);
     while (pending) {
         const u32 leader = __ffs(pending) - 1;
@@ -1040,11 +1047,11 @@ __device__ __forceinline__ int free_impl(const ouro_heap_view& v, void* ptr, u32
         const u32 nd = __ballot_sync(mask, st == OURO_ERR_DOUBLE_FREE);
         const u32 ni = __ballot_sync(mask, st == OURO_ERR_INVALID_HANDLE);
         if (nd && lane == (u32)(__ffs(nd) - 1)) {
-            atomicAdd(&v.ctr[2 * v.K + OURO_CTR_DOUBLE_FREE], (u64)__popc(nd));
+            atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_DOUBLE_FREE), (u64)__popc(nd));
             raise_err(v, OURO_ERR_DOUBLE_FREE);
         }
         if (ni && lane == (u32)(__ffs(ni) - 1)) {
-            atomicAdd(&v.ctr[2 * v.K + OURO_CTR_INVALID_FREE], (u64)__popc(ni));
+            atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_INVALID_FREE), (u64)__popc(ni));
             raise_err(v, OURO_ERR_INVALID_HANDLE);
         }
     }

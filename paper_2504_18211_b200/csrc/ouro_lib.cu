@@ -530,7 +530,7 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
     CK(cudaMemsetAsync(H->d_meta, 0, (size_t)N * 8, st));
     CK(cudaMemsetAsync(H->d_bitmap, 0, (size_t)N * g.Wmax * 8, st));
     CK(cudaMemsetAsync(H->d_assigned, 0, (size_t)K * 4, st));
-    CK(cudaMemsetAsync(H->d_ctr, 0, (size_t)(2 * K + OURO_CTR_N) * 8, st));
+    CK(cudaMemsetAsync(H->d_ctr, 0, (size_t)OURO_CTR_SHARDS * (2 * K + OURO_CTR_N) * 8, st));
     CK(cudaMemsetAsync(H->d_sticky, 0, 8, st));
     if (H->d_touched) CK(cudaMemsetAsync(H->d_touched, 0, g.heap / g.minp / 8 + 8, st));
     for (auto& q : H->hq) {
@@ -822,7 +822,7 @@ ouro_status ouro_heap_create(const ouro_config* cfg, int device, ouro_heap** out
     H->d_meta = static_cast<u64*>(dalloc(H, (size_t)g.N * 8));
     H->d_bitmap = static_cast<u64*>(dalloc(H, (size_t)g.N * g.Wmax * 8));
     H->d_assigned = static_cast<u32*>(dalloc(H, (size_t)g.K * 4));
-    H->d_ctr = static_cast<u64*>(dalloc(H, (size_t)(2 * g.K + OURO_CTR_N) * 8));
+    H->d_ctr = static_cast<u64*>(dalloc(H, (size_t)OURO_CTR_SHARDS * (2 * g.K + OURO_CTR_N) * 8));
     H->d_sticky = static_cast<u32*>(dalloc(H, 8));
     if (!H->d_heap || !H->d_meta || !H->d_bitmap || !H->d_assigned || !H->d_ctr || !H->d_sticky) return fail(OURO_ERR_CUDA);
     if (plan(H) != OURO_OK) return fail(OURO_ERR_CUDA);
@@ -918,9 +918,12 @@ ouro_status ouro_heap_stats(ouro_heap* H, ouro_stats* out, void* stream) {
     const ouro_status s = compute_digest(H, &dg, &hd, &qs, S(stream));
     if (s != OURO_OK) return s;
     const Geometry& g = H->g;
-    std::vector<u64> ctr(2 * g.K + OURO_CTR_N);
+    const size_t per = 2 * g.K + OURO_CTR_N;
+    std::vector<u64> shards(OURO_CTR_SHARDS * per), ctr(per, 0);
     u32 sticky[2];
-    CK(cudaMemcpy(ctr.data(), H->d_ctr, ctr.size() * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(shards.data(), H->d_ctr, shards.size() * 8, cudaMemcpyDeviceToHost));
+    for (size_t s = 0; s < OURO_CTR_SHARDS; ++s)
+        for (size_t i = 0; i < per; ++i) ctr[i] += shards[s * per + i];
     CK(cudaMemcpy(sticky, H->d_sticky, 8, cudaMemcpyDeviceToHost));
     std::memset(out, 0, sizeof(*out));
     out->num_classes = g.K;
