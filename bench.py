@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-threads", type=int, default=0)
     ap.add_argument("--sizes", default="", help="comma list overriding the config's sweep (experiments)")
+    ap.add_argument("--block", type=int, default=256, help="threads per block of the malloc/free launches")
+    ap.add_argument("--waves", type=int, default=0,
+                    help="persistent grid of WAVES x resident blocks (0: one thread per request)")
     return ap.parse_args()
 
 
@@ -273,6 +276,7 @@ def main():
         sizes = [int(x) for x in args.sizes.split(",")]
     hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
     heap = ob.Heap(hc, local)
+    ob.check(ob.lib().ouro_set_launch_shape(args.block, args.waves), "launch shape")
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
     res = torch.zeros(4, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

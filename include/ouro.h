@@ -171,6 +171,11 @@ ouro_status ouro_heap_reset(ouro_heap* heap, void* stream);
 /* Copy the POD device view (struct ouro_heap_view in ouro_device.cuh). */
 ouro_status ouro_heap_get_view(const ouro_heap* heap, void* view_out, size_t view_size);
 size_t ouro_heap_view_size(void);
+/* Launch shape of the alloc/free/churn launchers (process-wide): threads per
+ * block (multiple of 32, <= 256); waves: 0 = one thread per request, w >= 1 =
+ * persistent grid of w x resident blocks that grid-strides (measured slower,
+ * DESIGN.md section 4).  Default 256, 0. */
+ouro_status ouro_set_launch_shape(int block_threads, int waves);
 /* Debug mode: verify queue/bitmap invariants on every device op (CorruptionError
  * on mismatch).  Off by default; affects views fetched afterwards. */
 ouro_status ouro_heap_set_checks(ouro_heap* heap, int on);

@@ -188,7 +188,14 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 // equivalent to having polled that much earlier -- and a non-empty answer
 // still goes through the authoritative reservation RMW.
 // Entry: [63:8] time/256 ns, [7:3] queue tag, [2] no result yet, [1] in flight, [0] empty.
+// Shared memory is not initialised for kernels that do not call ouro_block_init,
+// so an entry counts only if its time lies in [now - window, now + kPollSkew]:
+// garbage that looks like a future entry is rejected, not taken as fresh.
 constexpr u64 kPollWindow = 32;  // x 256 ns = 8.2 us
+constexpr u64 kPollSkew = 2;     // entries written just after we read the clock
+__device__ __forceinline__ bool poll_recent(u64 now, u64 e, u64 window) {
+    return now - (e >> 8) + kPollSkew < window + kPollSkew;
+}
 __device__ __forceinline__ u64 gtime256() {
     u64 t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -211,13 +218,11 @@ static __device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 f
         const u64 now = gtime256();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
         const bool match = ((e >> 3) & 31u) == tag;
-        // signed: an entry written after we read the clock is fresh, not stale
-        const i64 age = (i64)(now - (e >> 8));
         if (match && !(e & 4u)) {
-            if (!(e & 2u) && age < (i64)kPollWindow) return (e & 1u) != 0;     // fresh
-            if ((e & 2u) && age < 4 * (i64)kPollWindow) return (e & 1u) != 0;  // being refreshed: reuse
+            if (!(e & 2u) && poll_recent(now, e, kPollWindow)) return (e & 1u) != 0;     // fresh
+            if ((e & 2u) && poll_recent(now, e, 4 * kPollWindow)) return (e & 1u) != 0;  // being refreshed: reuse
         }
-        if (match && (e & 6u) == 6u && age < 4 * (i64)kPollWindow) { __nanosleep(32); continue; }
+        if (match && (e & 6u) == 6u && poll_recent(now, e, 4 * kPollWindow)) { __nanosleep(32); continue; }
         const u64 mine = (match && !(e & 4u)) ? (e | 2u) : ((now << 8) | (tag << 3) | 6u);
         if (atomicCAS(slot, e, mine) != e) continue;
         const bool empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
@@ -233,9 +238,10 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
     const u64 tag = poll_tag(Q);
     u64* slot = poll_slot(tag);
     const u64 e = *reinterpret_cast<volatile u64*>(slot);
-    const i64 age = (i64)(gtime256() - (e >> 8));
+    const u64 now = gtime256();
     const u64 d = (e ^ (tag << 3)) & 0xFCu;  // 0: match, completed, idle; 2: match, completed, refreshing
-    if ((d == 0 && age < (i64)kPollWindow) || (d == 2 && age < 4 * (i64)kPollWindow)) return (e & 1u) != 0;
+    if ((d == 0 && poll_recent(now, e, kPollWindow)) || (d == 2 && poll_recent(now, e, 4 * kPollWindow)))
+        return (e & 1u) != 0;
     return observed_empty_slow(Q, floor, tag, slot);
 }
 
@@ -244,7 +250,7 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
     const u64 e = *reinterpret_cast<volatile u64*>(poll_slot(tag));
-    return ((e ^ (tag << 3)) & 0xFDu) == 1u && (i64)(gtime256() - (e >> 8)) < 4 * (i64)kPollWindow;
+    return ((e ^ (tag << 3)) & 0xFDu) == 1u && poll_recent(gtime256(), e, 4 * kPollWindow);
 }
 __device__ __forceinline__ void note_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
@@ -1124,6 +1130,17 @@ __device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, 
 }  // namespace ouro_dev
 
 // ---------------------------------------------------------------- public ----
+// Block-level allocator state.  ouro_block_init(), called by EVERY thread of the
+// block before any allocator call of the block, clears the block's retry-poll
+// cache ("poll combining" above).  Optional -- entries are validated by queue
+// tag and time -- but it keeps a block from reusing an observation another
+// kernel left in shared memory.  The C-ABI launchers call it.
+__device__ __forceinline__ void ouro_block_init() {
+    const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    if (t < 16) ouro_dev::poll_cache()[t] = 0;
+    __syncthreads();
+}
+
 // Compile-time variant entry points (fastest: no dispatch).
 // `lanes`: optional mask of the lanes of this warp that make the call together
 // (all of them must pass the same mask); 0 = whatever __activemask() reports.

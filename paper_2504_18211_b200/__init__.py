@@ -39,7 +39,8 @@ _LIB = None
 
 
 def lib_path() -> str:
-    return os.path.join(_HERE, "libouro_b200.so")
+    # OURO_B200_LIB: an alternative in-tree build (compile-time experiments)
+    return os.environ.get("OURO_B200_LIB") or os.path.join(_HERE, "libouro_b200.so")
 
 
 def lib() -> C.CDLL:
@@ -73,6 +74,7 @@ def _declare(L):
         "ouro_heap_get_view": (i32, [P, P, C.c_size_t]),
         "ouro_heap_view_size": (C.c_size_t, []),
         "ouro_heap_set_checks": (i32, [P, C.c_int]),
+        "ouro_set_launch_shape": (i32, [C.c_int, C.c_int]),
         "ouro_heap_config": (i32, [P, C.POINTER(Config), C.POINTER(Geometry)]),
         "ouro_heap_base": (u64, [P]),
         "ouro_page_region": (i32, [P, u32, C.POINTER(u64), C.POINTER(u64)]),

@@ -39,6 +39,25 @@ using ouro_host::Geometry;
 namespace {
 
 constexpr int kBlock = 256;
+// Launch shape of the malloc/free/churn drivers (one request per thread, requests
+// independent).  g_op_waves = 0: one thread per request (grid = n / block);
+// g_op_waves = w >= 1: persistent grid of w x (resident CTAs per SM) x SMs that
+// grid-strides over the requests.  Persistent CTAs keep their shared-memory poll
+// state (ouro_device.cuh "poll combining") across requests, so an OOM storm pays
+// one count RMW+undo per CTA instead of per warp.
+int g_op_block = 256;
+int g_op_waves = 0;
+template <class Kern>
+unsigned op_grid(Kern kern, u64 n) {
+    const u64 need = std::max<u64>(1, (n + g_op_block - 1) / g_op_block);
+    if (g_op_waves <= 0) return (unsigned)need;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, g_op_block, 0);
+    const u64 cap = (u64)std::max(1, per_sm) * (u64)std::max(1, sms) * (u64)g_op_waves;
+    return (unsigned)std::min(need, cap);
+}
 
 __host__ __device__ inline u64 mix64h(u64 x) {
     x += 0x9E3779B97F4A7C15ull;
@@ -110,18 +129,21 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 // more than the extra warps gain, profiles/r1_ncu_summary.md.)
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const u32* sizes, void** out) {
-    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-    const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
-    if (i >= n) return;
-    const u64 sz = sizes ? sizes[i] : uniform;
-    out[i] = ouro_malloc_t<KIND, FL>(v, sz, nullptr, lanes);
+    ouro_block_init();
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
+        const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
+        if (i < n) out[i] = ouro_malloc_t<KIND, FL>(v, sizes ? sizes[i] : uniform, nullptr, lanes);
+    }
 }
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_free(ouro_heap_view v, u64 n, void* const* ptrs) {
-    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-    const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
-    if (i >= n) return;
-    ouro_free_t<KIND, FL>(v, ptrs[i], lanes);
+    ouro_block_init();
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
+        const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
+        if (i < n) ouro_free_t<KIND, FL>(v, ptrs[i], lanes);
+    }
 }
 
 __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p) {
@@ -216,10 +238,8 @@ __global__ void k_audit_neighbours(u64 m, const u64* offs, const u64* lens, u64*
 
 // ------------------------------------------------------------------- churn ----
 template <int KIND, int FL>
-__global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
-                                                  uint8_t* touched, u64* res) {
-    const u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x;
-    const bool in = t < n;
+__device__ __forceinline__ void churn_slot(const ouro_heap_view& v, u64 t, bool in, u32 r, u64 seed, void** slots,
+                                           uint8_t* touched, u64* res) {
     const u64 h = mix64h(seed ^ (t << 32) ^ r);
     void* s = in ? slots[t] : nullptr;
     const bool do_free = in && s && (h & 1);
@@ -259,10 +279,19 @@ __global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r
         if (e) atomicAdd(&res[4], (u64)__popc(e));
     }
 }
+template <int KIND, int FL>
+__global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
+                                                  uint8_t* touched, u64* res) {
+    ouro_block_init();
+    const u64 stride = (u64)gridDim.x * blockDim.x;
+    for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t - threadIdx.x % 32 < n; t += stride)
+        churn_slot<KIND, FL>(v, t, t < n, r, seed, slots, touched, res);
+}
 
 // --------------------------------------------------------- op-script runner ----
 template <int KIND, int FL>
 __global__ void k_script(ouro_heap_view v, const ouro_script_step* steps, u32 nsteps, u64* out_off, int* out_st) {
+    ouro_block_init();
     const u32 lane = threadIdx.x;
     for (u32 s = 0; s < nsteps; ++s) {
         const ouro_script_step& st = steps[s];
@@ -429,15 +458,15 @@ __global__ void k_atom_same_lane(u64* a, u32 iters) {
 
 template <int K, int F>
 void launch_alloc(ouro_heap* H, u64 n, u64 uni, const u32* sizes, void** out, cudaStream_t st) {
-    k_alloc<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, uni, sizes, out);
+    k_alloc<K, F><<<op_grid(k_alloc<K, F>, n), g_op_block, 0, st>>>(H->view, n, uni, sizes, out);
 }
 template <int K, int F>
 void launch_free(ouro_heap* H, u64 n, void* const* p, cudaStream_t st) {
-    k_free<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, p);
+    k_free<K, F><<<op_grid(k_free<K, F>, n), g_op_block, 0, st>>>(H->view, n, p);
 }
 template <int K, int F>
 void launch_churn(ouro_heap* H, u64 n, u32 r, u64 seed, void** slots, u64* res, cudaStream_t st) {
-    k_churn<K, F><<<grid_for(n), kBlock, 0, st>>>(H->view, n, r, seed, slots, H->d_touched, res);
+    k_churn<K, F><<<op_grid(k_churn<K, F>, n), g_op_block, 0, st>>>(H->view, n, r, seed, slots, H->d_touched, res);
 }
 template <int K, int F>
 void launch_script(ouro_heap* H, const ouro_script_step* s, u32 n, u64* o, int* st) {
@@ -852,6 +881,13 @@ ouro_status ouro_heap_reset(ouro_heap* H, void* stream) {
 }
 
 size_t ouro_heap_view_size(void) { return sizeof(ouro_heap_view); }
+
+ouro_status ouro_set_launch_shape(int block_threads, int waves) {
+    if (block_threads < 32 || block_threads > kBlock || block_threads % 32 || waves < 0) return OURO_ERR_USAGE;
+    g_op_block = block_threads;
+    g_op_waves = waves;
+    return OURO_OK;
+}
 
 ouro_status ouro_heap_set_checks(ouro_heap* H, int on) {
     if (!H) return OURO_ERR_USAGE;
