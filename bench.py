@@ -375,9 +375,10 @@ def main():
     # copies are inside the timed region.
     e2e_ms, e2e_ok = 0.0, 0
     e2e_reps = []
-    h_sizes = [torch.full((n,), s, dtype=torch.int32).pin_memory() for s in sizes]
+    # 16-bit request sizes (ouro_launch_alloc_u16): every valid request is <= 8 KiB
+    h_sizes = [torch.full((n,), s, dtype=torch.int16).pin_memory() for s in sizes]
     h_res = torch.zeros(len(sizes), dtype=torch.int64).pin_memory()
-    d_sizes = [torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(2)]
+    d_sizes = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(2)]
     d_res = torch.zeros(len(sizes), dtype=torch.int64, device="cuda")
     s_copy, s_comp = torch.cuda.Stream(), torch.cuda.Stream()
     for rep in range(args.warmup + args.steps):  # warm-up passes, then K timed passes
@@ -486,9 +487,9 @@ def main():
                              "max_retries rounds, not on the RMW chain; per_size[*].alloc_roofline_frac "
                              "gives the fraction where all threads are served"},
         "e2e": {"value": e2e_ok / (e2e_ms / 1e3) * world, "unit": "pairs/s",
-                "h2d_bytes_per_step": 4 * n * len(sizes), "d2h_bytes_per_step": 8 * len(sizes),
+                "h2d_bytes_per_step": 2 * n * len(sizes), "d2h_bytes_per_step": 8 * len(sizes),
                 "ms_per_step_median": statistics.median(e2e_reps), "steps": len(e2e_reps),
-                "path": "ouro_launch_alloc/count/free (C-ABI) per size; per-thread request sizes copied H2D "
+                "path": "ouro_launch_alloc_u16/count/free (C-ABI) per size; per-thread 16-bit request sizes copied H2D "
                         "from pinned host memory on a copy stream (overlapping the previous size's kernels), "
                         "success counts copied D2H, all inside the timed region"},
         "gpu_launches": launches,

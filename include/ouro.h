@@ -196,6 +196,11 @@ ouro_status ouro_heap_last_error(ouro_heap* heap, uint32_t* first, uint32_t* mas
  * (size_i = d_sizes ? d_sizes[i] : uniform_bytes).  NULL on OOM/TooLarge. */
 ouro_status ouro_launch_alloc(ouro_heap* heap, uint64_t n, uint64_t uniform_bytes,
                               const uint32_t* d_sizes, void** d_out, void* stream);
+/* Same with 16-bit request sizes (every valid request is <= max_page_bytes <=
+ * 65535 B; a request that does not fit 16 bits is TooLarge anyway): half the
+ * bytes to move when the request array comes from the host. */
+ouro_status ouro_launch_alloc_u16(ouro_heap* heap, uint64_t n, const uint16_t* d_sizes, void** d_out,
+                                  void* stream);
 /* One device thread per slot: ouro_free(d_ptrs[i]) (NULL slots skipped). */
 ouro_status ouro_launch_free(ouro_heap* heap, uint64_t n, void* const* d_ptrs, void* stream);
 /* Fill every live page (its full page_region) with the slot/iteration-keyed

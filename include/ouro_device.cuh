@@ -245,6 +245,58 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
     return observed_empty_slow(Q, floor, tag, slot);
 }
 
+// Failed retry rounds on a group leader: backoff, then the
+// block-combined poll of the class queue (and, for the chunk kind, of the pool);
+// stops when a poll sees work (returns false) or when the budget is spent
+// (returns true: OutOfMemory).  *attempt counts rounds as the oracle does.
+// FenceRetry is specialised so a round is the fence plus a shared-memory read, a
+// clock read and a 32-bit age check (the retry rounds of an OOM storm --
+// 2^15 leaders x 63 rounds -- are bound by instruction issue, tools/round_loop.cu).
+__device__ __forceinline__ bool poll_fresh32(u64 e, u32 key, u32 now, bool* empty) {
+    const u32 age = now - (u32)(e >> 8) + (u32)kPollSkew;
+    const u32 d = ((u32)e ^ key) & 0xFCu;
+    *empty = (e & 1u) != 0;
+    return (d == 0u && age < (u32)(kPollWindow + kPollSkew)) || (d == 2u && age < (u32)(4 * kPollWindow + kPollSkew));
+}
+__device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
+                                            i64 pfloor, u32* attempt) {
+    u32 a = *attempt;
+    const u32 maxr = v.max_retries;
+    if (v.backoff == OURO_BACKOFF_SLEEP) {
+        for (;;) {
+            if (++a >= maxr) { *attempt = a; return true; }
+            backoff(v, a);
+            if (!observed_empty(Q, 0) || (P && !observed_empty(P, pfloor))) break;
+        }
+        *attempt = a;
+        return false;
+    }
+    const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
+    u64* sq = poll_slot(tq);
+    u64* sp = poll_slot(tp);
+    const u32 kq = (u32)(tq << 3), kp = (u32)(tp << 3);
+    for (;;) {
+        if (++a >= maxr) { *attempt = a; return true; }
+#if OURO_FENCE_SCOPE_GPU
+        asm volatile("fence.sc.gpu;" ::: "memory");
+#else
+        asm volatile("fence.sc.cta;" ::: "memory");
+#endif
+        const u32 now = (u32)gtime256();
+        bool empty;
+        if (!poll_fresh32(*reinterpret_cast<volatile u64*>(sq), kq, now, &empty)) [[unlikely]]
+            empty = observed_empty_slow(Q, 0, tq, sq);
+        if (!empty) break;
+        if (P) {
+            if (!poll_fresh32(*reinterpret_cast<volatile u64*>(sp), kp, now, &empty)) [[unlikely]]
+                empty = observed_empty_slow(P, pfloor, tp, sp);
+            if (!empty) break;
+        }
+    }
+    *attempt = a;
+    return false;
+}
+
 // Did this block recently see the queue empty?  (hint only: it just turns the
 // first try's RMW into load-then-RMW, which reserves exactly the same.)
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
@@ -838,14 +890,7 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         // oracle's (one failed try per round, OOM after max_retries).
         const u32 leader = __ffs(todo) - 1, rem = __popc(todo);
         u32 a = attempt, oom = 0;
-        if (lane == leader) {
-            for (;;) {
-                ++a;
-                if (a >= v.max_retries) { oom = 1; break; }
-                backoff(v, a);
-                if (!observed_empty(v.q + k, 0)) break;
-            }
-        }
+        if (lane == leader) oom = fail_rounds(v, v.q + k, nullptr, 0, &a) ? 1u : 0u;
         a = __shfl_sync(mask, a, leader);
         oom = __shfl_sync(mask, oom, leader);
         retries += (u64)rem * (a - attempt);
@@ -947,14 +992,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         }
         // both empty: failed rounds on the leader alone until a poll sees work
         u32 a = attempt, oom = 0;
-        if (lane == leader) {
-            for (;;) {
-                ++a;
-                if (a >= v.max_retries) { oom = 1; break; }
-                backoff(v, a);
-                if (!observed_empty(v.q + k, 0) || !observed_empty(v.q + pool, v.floor_F)) break;
-            }
-        }
+        if (lane == leader) oom = fail_rounds(v, v.q + k, v.q + pool, v.floor_F, &a) ? 1u : 0u;
         a = __shfl_sync(mask, a, leader);
         oom = __shfl_sync(mask, oom, leader);
         retries += (u64)n * (a - attempt);

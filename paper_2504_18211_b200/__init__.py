@@ -82,6 +82,7 @@ def _declare(L):
         "ouro_heap_digest": (i32, [P, C.POINTER(Digest), P]),
         "ouro_heap_last_error": (i32, [P, C.POINTER(u32), C.POINTER(u32), C.c_int]),
         "ouro_launch_alloc": (i32, [P, u64, u64, P, P, P]),
+        "ouro_launch_alloc_u16": (i32, [P, u64, P, P, P]),
         "ouro_launch_free": (i32, [P, u64, P, P]),
         "ouro_launch_write": (i32, [P, u64, P, u64, u32, P]),
         "ouro_launch_verify": (i32, [P, u64, P, u64, u32, P, P]),
@@ -341,6 +342,10 @@ class Heap:
 
     # ---- driver phases (device buffers: torch tensors or raw pointers) ----
     def launch_alloc(self, n, out_ptrs, size=0, sizes=None, stream=None):
+        """sizes: optional device array of per-slot request sizes, int32 or int16/uint16."""
+        if sizes is not None and getattr(sizes, "element_size", lambda: 4)() == 2:
+            check(lib().ouro_launch_alloc_u16(self._h, n, _ptr(sizes), _ptr(out_ptrs), _stream(stream)), "alloc")
+            return
         check(lib().ouro_launch_alloc(self._h, n, size, _ptr(sizes), _ptr(out_ptrs), _stream(stream)), "alloc")
 
     def launch_free(self, n, ptrs, stream=None):

@@ -127,8 +127,8 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 // ------------------------------------------------------------ driver phases ----
 // (Forcing 32 registers for 8 blocks/SM was measured slower: the spills cost
 // more than the extra warps gain, profiles/r1_ncu_summary.md.)
-template <int KIND, int FL>
-__global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const u32* sizes, void** out) {
+template <int KIND, int FL, class SZ = u32>
+__global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const SZ* sizes, void** out) {
     ouro_block_init();
     const u64 stride = (u64)gridDim.x * blockDim.x;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
@@ -459,6 +459,10 @@ __global__ void k_atom_same_lane(u64* a, u32 iters) {
 template <int K, int F>
 void launch_alloc(ouro_heap* H, u64 n, u64 uni, const u32* sizes, void** out, cudaStream_t st) {
     k_alloc<K, F><<<op_grid(k_alloc<K, F>, n), g_op_block, 0, st>>>(H->view, n, uni, sizes, out);
+}
+template <int K, int F>
+void launch_alloc16(ouro_heap* H, u64 n, const uint16_t* sizes, void** out, cudaStream_t st) {
+    k_alloc<K, F, uint16_t><<<op_grid(k_alloc<K, F, uint16_t>, n), g_op_block, 0, st>>>(H->view, n, 0, sizes, out);
 }
 template <int K, int F>
 void launch_free(ouro_heap* H, u64 n, void* const* p, cudaStream_t st) {
@@ -995,6 +999,14 @@ ouro_status ouro_launch_alloc(ouro_heap* H, uint64_t n, uint64_t uniform_bytes, 
     if (!H || !d_out) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
     OURO_VSWITCH(H, launch_alloc, H, n, uniform_bytes, d_sizes, d_out, S(stream));
+    CK(cudaGetLastError());
+    return OURO_OK;
+}
+
+ouro_status ouro_launch_alloc_u16(ouro_heap* H, uint64_t n, const uint16_t* d_sizes, void** d_out, void* stream) {
+    if (!H || !d_out || !d_sizes) return OURO_ERR_USAGE;
+    if (n == 0) return OURO_OK;
+    OURO_VSWITCH(H, launch_alloc16, H, n, d_sizes, d_out, S(stream));
     CK(cudaGetLastError());
     return OURO_OK;
 }

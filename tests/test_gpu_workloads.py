@@ -255,3 +255,37 @@ def test_acceptance_6_page_flat(cuda, flavor):
     with ob.Heap(_hc(0, flavor, 64 << 20)) as h:
         t = [h.run_trial(1024, s, iterations=10, seed=s).mean_subsequent_ms for s in range(1000, 8001, 1000)]
         assert max(t) / min(t) <= 3.0, t
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=IDS)
+def test_alloc_u16_sizes_match_u32(cuda, variant):
+    """ouro_launch_alloc_u16: 16-bit request sizes give exactly the 32-bit launcher's
+    results (success pattern, classes, TooLarge for 0 and > 8 KiB)."""
+    torch = cuda
+    n = 1 << 14
+    g = torch.Generator().manual_seed(5)
+    sz = torch.randint(0, 9000, (n,), generator=g, dtype=torch.int32)
+    sz[::97] = 65535
+    sz[::89] = 0
+    res = {}
+    for dt in (torch.int32, torch.int16):
+        # 1 GiB: no class runs out (the page kind's 8 KiB class holds ~100 MiB), so the
+        # success pattern is interleaving-independent
+        with ob.Heap(_hc(*variant, 1 << 30)) as h:
+            ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+            d = sz.to(dt).cuda() if dt == torch.int32 else sz.to(torch.int32).to(torch.int16).cuda()
+            h.launch_alloc(n, ptrs, sizes=d)
+            torch.cuda.synchronize()
+            live = (ptrs != 0).cpu()
+            s = h.stats()
+            res[dt] = (live, s.bad_sizes if hasattr(s, "bad_sizes") else None,
+                       [s.cls[k].live_pages for k in range(s.num_classes)])
+            a = h.audit(n, ptrs)
+            assert a.overlaps == 0 and a.misaligned == 0 and a.live == int(live.sum())
+            h.launch_free(n, ptrs)
+            torch.cuda.synchronize()
+            assert h.last_error()[0] == 0
+    assert torch.equal(res[torch.int32][0], res[torch.int16][0])
+    assert res[torch.int32][2] == res[torch.int16][2]
+    bad = (sz == 0) | (sz > 8192)
+    assert not res[torch.int16][0][bad].any()
