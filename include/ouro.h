@@ -186,6 +186,11 @@ uint64_t ouro_heap_base(const ouro_heap* heap); /* device address of heap byte 0
 ouro_status ouro_page_region(ouro_heap* heap, uint32_t h, uint64_t* offset, uint64_t* len);
 /* stats; exact at quiescence. */
 ouro_status ouro_heap_stats(ouro_heap* heap, ouro_stats* out, void* stream);
+/* Debug/test: queue qi's {count, head ticket, VirtualList head link, tail link}
+ * (links {seq:32|chunk:32}); synchronises the device. */
+ouro_status ouro_heap_queue_links(ouro_heap* heap, uint32_t qi, uint64_t out[4]);
+/* Debug/test: queue qi's dequeue-side VirtualList ring (256 links). */
+ouro_status ouro_heap_vl_ring(ouro_heap* heap, uint32_t qi, uint64_t out[256]);
 /* Canonical digest; call at quiescence. */
 ouro_status ouro_heap_digest(ouro_heap* heap, ouro_digest* out, void* stream);
 /* Sticky device error word; clear != 0 resets it. */

@@ -55,7 +55,14 @@ typedef struct ouro_queue_dev {
      * seq matches (a segment cannot retire while a caller still needs it). */
 #define OURO_VL_RECENT 256
     ouro_u64 vl_recent[OURO_VL_RECENT];
-    uint8_t pad5[3 * OURO_HOT_STRIDE - 80 - 8 * OURO_VL_RECENT];
+    /* Dequeue-side accelerator: links of the segments at and ahead of the head at
+     * [seq % OURO_VL_RECENT], kept ahead of consumption by the dequeuer that starts
+     * each segment (ouro_device.cuh vl_extend_ring); walkers record every hop they
+     * validate.  Same rule: used only on a seq match. */
+    ouro_u64 vl_deq[OURO_VL_RECENT];
+    uint32_t vl_front;                 /* highest seq recorded contiguously in vl_deq */
+    uint32_t vl_pad;
+    uint8_t pad5[5 * OURO_HOT_STRIDE - 88 - 16 * OURO_VL_RECENT];
 } ouro_queue_dev;
 
 /* Counter indices in ctr[] (after 2*K per-class retries/ooms). */

@@ -180,17 +180,19 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 // ------------------------------------------------------- count / tickets ----
 // Per-block poll combining for retry rounds.  Retrying warps (OOM storms:
 // ~10^6 lanes x max_retries rounds) would otherwise all poll the same count
-// word, and same-address loads serialise in one L2 slice.  Within a block the
-// first warp that needs a fresh observation of a queue becomes the poller (CAS
-// marks the entry in flight); while a refresh is in flight the other warps
-// reuse the previous completed observation (at most 4 windows old) instead of
-// waiting for L2.  Every observation is therefore at most ~33 us old --
-// equivalent to having polled that much earlier -- and a non-empty answer
-// still goes through the authoritative reservation RMW.
-// Entry: [63:8] time/256 ns, [7:3] queue tag, [2] no result yet, [1] in flight, [0] empty.
-// Shared memory is not initialised for kernels that do not call ouro_block_init,
-// so an entry counts only if its time lies in [now - window, now + kPollSkew]:
-// garbage that looks like a future entry is rejected, not taken as fresh.
+// word, and same-address loads serialise in one L2 slice.  Within a block one
+// warp at a time polls a queue's count (CAS marks the entry in flight) and
+// every warp of the block waiting for an observation shares the result.
+// Each retry round needs its OWN observation: poll_after() accepts only a poll
+// issued strictly after the observation the warp's previous round used (for
+// the first round: after its failed try), so OutOfMemory is declared only
+// after max_retries distinct observations of "no page obtainable"
+// -- a queue that refills while a warp retries is seen by its next round.
+// Entry: [63:8] poll issue time / 256 ns, [7:3] queue tag, [2] no result yet,
+// [1] in flight, [0] empty.  Shared memory is not initialised for kernels that
+// do not call ouro_block_init, so an entry counts only if its time lies in
+// [now - window, now + kPollSkew]: garbage that looks like a future entry is
+// rejected.
 constexpr u64 kPollWindow = 32;  // x 256 ns = 8.2 us
 constexpr u64 kPollSkew = 2;     // entries written just after we read the clock
 __device__ __forceinline__ bool poll_recent(u64 now, u64 e, u64 window) {
@@ -212,86 +214,64 @@ __device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) {
 }
 __device__ __forceinline__ u64* poll_slot(u64 tag) { return poll_cache() + (tag & 15); }
 
-// Slow path: become the poller, or wait for / reuse an in-flight poll.
-static __device__ __noinline__ bool observed_empty_slow(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot) {
-    for (int spins = 0; spins < 256; ++spins) {
+// An observation of (count - floor <= 0) issued strictly after tick `after`;
+// *when receives its issue tick.  Reuses a completed poll of this block, waits
+// for one in flight, or issues one.
+static __device__ __noinline__ bool poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot, u64 after,
+                                               u64* when) {
+    for (int spins = 0; spins < 4096; ++spins) {
         const u64 now = gtime256();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
-        const bool match = ((e >> 3) & 31u) == tag;
-        if (match && !(e & 4u)) {
-            if (!(e & 2u) && poll_recent(now, e, kPollWindow)) return (e & 1u) != 0;     // fresh
-            if ((e & 2u) && poll_recent(now, e, 4 * kPollWindow)) return (e & 1u) != 0;  // being refreshed: reuse
+        const bool mine_tag = ((e >> 3) & 31u) == tag && poll_recent(now, e, 4 * kPollWindow);
+        const u64 t = e >> 8;
+        if (mine_tag && (i64)(t - after) > 0) {
+            if (!(e & 6u)) { *when = t; return (e & 1u) != 0; }  // completed, issued after `after`
+            if (e & 2u) { __nanosleep(32); continue; }            // in flight, issued after: wait
         }
-        if (match && (e & 6u) == 6u && poll_recent(now, e, 4 * kPollWindow)) { __nanosleep(32); continue; }
-        const u64 mine = (match && !(e & 4u)) ? (e | 2u) : ((now << 8) | (tag << 3) | 6u);
-        if (atomicCAS(slot, e, mine) != e) continue;
+        if (mine_tag && (e & 2u)) { __nanosleep(32); continue; }  // an older poll in flight
+        if ((i64)(now - after) <= 0) { __nanosleep(64); continue; }  // our poll must start later
+        const u64 keep = mine_tag ? (e & 5u) : 4u;  // old result stays as a hint
+        if (atomicCAS(slot, e, (now << 8) | (tag << 3) | 2u | keep) != e) continue;
         const bool empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
-        atomicExch(slot, (gtime256() << 8) | (tag << 3) | (empty ? 1u : 0u));
+        atomicExch(slot, (now << 8) | (tag << 3) | (empty ? 1u : 0u));
+        *when = now;
         return empty;
     }
+    const u64 now = gtime256();
+    *when = now;
     return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
 }
 
-// true: the queue was observed (count - floor <= 0) recently.  Fast path (a
-// fresh completed entry, or one being refreshed): one LDS, one clock read.
+// Pre-check before a reservation RMW (hint: the RMW decides).  One LDS, one
+// clock read when this block has a recent completed observation.
 __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
     const u64 tag = poll_tag(Q);
     u64* slot = poll_slot(tag);
     const u64 e = *reinterpret_cast<volatile u64*>(slot);
     const u64 now = gtime256();
-    const u64 d = (e ^ (tag << 3)) & 0xFCu;  // 0: match, completed, idle; 2: match, completed, refreshing
-    if ((d == 0 && poll_recent(now, e, kPollWindow)) || (d == 2 && poll_recent(now, e, 4 * kPollWindow)))
-        return (e & 1u) != 0;
-    return observed_empty_slow(Q, floor, tag, slot);
+    if (((e ^ (tag << 3)) & 0xFCu) == 0u && poll_recent(now, e, kPollWindow)) return (e & 1u) != 0;
+    u64 w;
+    return poll_after(Q, floor, tag, slot, now - kPollWindow, &w);
 }
 
-// Failed retry rounds on a group leader: backoff, then the
-// block-combined poll of the class queue (and, for the chunk kind, of the pool);
-// stops when a poll sees work (returns false) or when the budget is spent
-// (returns true: OutOfMemory).  *attempt counts rounds as the oracle does.
-// FenceRetry is specialised so a round is the fence plus a shared-memory read, a
-// clock read and a 32-bit age check (the retry rounds of an OOM storm --
-// 2^15 leaders x 63 rounds -- are bound by instruction issue, tools/round_loop.cu).
-__device__ __forceinline__ bool poll_fresh32(u64 e, u32 key, u32 now, bool* empty) {
-    const u32 age = now - (u32)(e >> 8) + (u32)kPollSkew;
-    const u32 d = ((u32)e ^ key) & 0xFCu;
-    *empty = (e & 1u) != 0;
-    return (d == 0u && age < (u32)(kPollWindow + kPollSkew)) || (d == 2u && age < (u32)(4 * kPollWindow + kPollSkew));
-}
+// Failed retry rounds on a group leader: backoff, then a
+// block-combined observation of the class queue (and, for the chunk kind, of
+// the pool) issued after the previous round's; stops when one sees work
+// (returns false) or when the budget is spent (returns true: OutOfMemory).
+// *attempt counts rounds as the oracle does.
 __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
                                             i64 pfloor, u32* attempt) {
     u32 a = *attempt;
     const u32 maxr = v.max_retries;
-    if (v.backoff == OURO_BACKOFF_SLEEP) {
-        for (;;) {
-            if (++a >= maxr) { *attempt = a; return true; }
-            backoff(v, a);
-            if (!observed_empty(Q, 0) || (P && !observed_empty(P, pfloor))) break;
-        }
-        *attempt = a;
-        return false;
-    }
     const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
     u64* sq = poll_slot(tq);
     u64* sp = poll_slot(tp);
-    const u32 kq = (u32)(tq << 3), kp = (u32)(tp << 3);
+    u64 lq = gtime256(), lp = lq;  // the failed try happened before this tick
     for (;;) {
         if (++a >= maxr) { *attempt = a; return true; }
-#if OURO_FENCE_SCOPE_GPU
-        asm volatile("fence.sc.gpu;" ::: "memory");
-#else
-        asm volatile("fence.sc.cta;" ::: "memory");
-#endif
-        const u32 now = (u32)gtime256();
-        bool empty;
-        if (!poll_fresh32(*reinterpret_cast<volatile u64*>(sq), kq, now, &empty)) [[unlikely]]
-            empty = observed_empty_slow(Q, 0, tq, sq);
-        if (!empty) break;
-        if (P) {
-            if (!poll_fresh32(*reinterpret_cast<volatile u64*>(sp), kp, now, &empty)) [[unlikely]]
-                empty = observed_empty_slow(P, pfloor, tp, sp);
-            if (!empty) break;
-        }
+        backoff(v, a);
+        if (!poll_after(Q, 0, tq, sq, lq, &lq)) break;
+        if (P && !poll_after(P, pfloor, tp, sp, lp, &lp)) break;
     }
     *attempt = a;
     return false;
@@ -304,12 +284,15 @@ __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 e = *reinterpret_cast<volatile u64*>(poll_slot(tag));
     return ((e ^ (tag << 3)) & 0xFDu) == 1u && poll_recent(gtime256(), e, 4 * kPollWindow);
 }
-__device__ __forceinline__ void note_empty(const ouro_queue_dev* Q) {
+// A reservation RMW issued after tick t0 found the queue empty: record it as an
+// observation issued at t0 (never later than the RMW itself).
+__device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u64 t0) {
     const u64 tag = poll_tag(Q);
     u64* slot = poll_slot(tag);
     const u64 e = *reinterpret_cast<volatile u64*>(slot);
     if ((e & 2u) && ((e >> 3) & 31u) == tag) return;  // a poll is in flight: leave it
-    atomicCAS(slot, e, (gtime256() << 8) | (tag << 3) | 1u);
+    if (((e >> 3) & 31u) == tag && !(e & 4u) && (i64)((e >> 8) - t0) >= 0) return;  // newer already
+    atomicCAS(slot, e, (t0 << 8) | (tag << 3) | 1u);
 }
 
 // Count reservation (broker-queue style).
@@ -329,12 +312,13 @@ __device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, 
     } else if (hint_empty(Q) && (i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
         return 0;
     }
+    const u64 t0 = gtime256();
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
     if (got < n) {
         atomicAdd((u64*)&Q->count, (u64)(n - got));
-        note_empty(Q);
+        note_empty(Q, t0);
     }
     return got;
 }
@@ -513,7 +497,9 @@ __device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_de
     Spin sp;
     for (;;) {
         const u64 r = ld_rlx(&Q->vl_recent[s % OURO_VL_RECENT]);
+        const u64 d = from_tail ? NONE_LINK : ld_rlx(&Q->vl_deq[s % OURO_VL_RECENT]);  // issued together
         if (lchk(r) != NONE && lseq(r) == (u32)s) { *out = lchk(r); return true; }
+        if (lchk(d) != NONE && lseq(d) == (u32)s) { *out = lchk(d); return true; }
         if (from_tail && (lchk(r) == NONE || (int)((u32)s - lseq(r)) > 0)) {  // creator of s not done yet
             if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
             continue;
@@ -532,6 +518,7 @@ __device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_de
                 if ((int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0 || nx == NONE_LINK) { ok = false; break; }
                 cur = lchk(nx);
                 ++i;
+                if (!from_tail) st_rlx(&Q->vl_deq[i % OURO_VL_RECENT], nx);  // record the hop
             }
             if (ok) { *out = cur; return true; }
         }
@@ -548,30 +535,108 @@ __device__ __forceinline__ void vl_tail_max(ouro_queue_dev* Q, u64 l) {
     }
 }
 
-// Warp-collective: advance head over fully retired segments (counter ==
-// S'+1), returning each to the segment source in order.  `who` drives it.
+// Keep the dequeue-side ring ahead of the dequeuers.  The dequeuer that takes
+// the first slot of segment s makes sure segment T = s + OURO_VL_RECENT - kVlSlack
+// is recorded: it walks from the frontier (vl_front, the highest seq recorded
+// contiguously, advanced with atomicMax -- no CAS loop, racing extenders write
+// the same entries) to T, normally one hop.  If the frontier entry is gone (its
+// slot recycled) or the head overtook it, the walk restarts at the head link.
+// T's slot belonged to segment s - kVlSlack, which only a straggler still needs.
+// Each hop's link is read from a segment ahead of the head and validated against
+// the head afterwards, as in vl_locate.
+constexpr u32 kVlSlack = 128;  // in-flight tickets span a few dozen segments (measured: 32 evicted live entries)
+__device__ __forceinline__ void vl_extend_ring(const ouro_heap_view& v, ouro_queue_dev* Q, u32 s) {
+    const u32 T = s + OURO_VL_RECENT - kVlSlack;
+    const u32 f = *reinterpret_cast<volatile const u32*>(&Q->vl_front);
+    if ((int)(f - T) >= 0) return;  // already recorded
+    u64 e[4];
+#pragma unroll
+    for (u32 d = 0; d < 4; ++d) e[d] = ld_rlx(&Q->vl_deq[(f - d) % OURO_VL_RECENT]);
+    const u64 h = ld_rlx(&Q->vl_head);
+    if (lchk(h) == NONE) return;
+    u32 i = lseq(h), cur = lchk(h);
+#pragma unroll
+    for (u32 d = 0; d < 4; ++d) {  // the frontier entry, or one just below it
+        if (lchk(e[d]) != NONE && lseq(e[d]) == f - d && (int)(f - d - lseq(h)) >= 0) {
+            i = f - d;
+            cur = lchk(e[d]);
+            break;
+        }
+    }
+    while (i != T) {
+        const u64 nx = ld_rlx(chunk_words(v, cur));
+        if (nx == NONE_LINK || (int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0) break;
+        cur = lchk(nx);
+        ++i;
+        st_rlx(&Q->vl_deq[i % OURO_VL_RECENT], nx);
+    }
+    if ((int)(i - f) > 0) {
+        __threadfence();  // the recorded entries before the frontier that names them
+        atomicMax(&Q->vl_front, i);
+    }
+}
+
+// Warp-collective retirement, batched: lane l looks at segment head + l (its
+// chunk from the dequeue-side ring, lane 0 from the head link), the run of
+// retired segments (counter == S'+1, successor linked) from the head moves the
+// head with ONE CAS, and the run's chunks go back to the segment source with
+// one warp enqueue (in segment order).  Only the CAS winner continues; a loser
+// stops.  A segment c completed while the head was behind it is not lost: its
+// completer increments c's counter, fences, then reads the head (vl_add); the
+// advancer CASes the head, fences, then reads the counters -- with both fences
+// seq-cst, at least one sees the other's write (store-buffering litmus).
 __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
                                                u32 lane, u32 who) {
     const u32 full = (u32)v.S_vl + 1u;
+    const u32 L = __popc(mask), li = __popc(mask & lanemask_lt());
     for (;;) {
-        u32 go = 0, ch = NONE, released = 0;
-        if (lane == who) {
-            u64 h = ld_rlx(&Q->vl_head);
-            ch = lchk(h);
-            if (ch != NONE && ld_rlx32(vl_counter(v, ch)) == full) {
-                const u64 nx = ld_rlx(chunk_words(v, ch));
-                if (nx != NONE_LINK) {
-                    go = 1;
-                    if (atomicCAS((u64*)&Q->vl_head, h, nx) == h) released = 1;
-                }
-            }
+        u64 h = 0;
+        if (lane == who) h = ld_rlx(&Q->vl_head);
+        h = shfl64(mask, h, who);
+        if (lchk(h) == NONE) return;
+        const u32 seq = lseq(h) + li;
+        u32 c = NONE;
+        if (li == 0) {
+            c = lchk(h);
+        } else {
+            const u64 e = ld_rlx(&Q->vl_deq[seq % OURO_VL_RECENT]);
+            if (lchk(e) != NONE && lseq(e) == seq) c = lchk(e);
         }
-        go = __shfl_sync(mask, go, who);
-        if (!go) return;
-        released = __shfl_sync(mask, released, who);
-        if (released) {
-            arr_enqueue(v, v.q + Q->seg_src, mask, lane, 1u << who, ch, true);
-            if (lane == who) seg_count(Q, -1);
+        u64 nx = NONE_LINK;
+        bool done = false;
+        if (c != NONE && ld_rlx32(vl_counter(v, c)) == full) {
+            nx = ld_rlx(chunk_words(v, c));
+            done = nx != NONE_LINK && lseq(nx) == seq + 1u;
+        }
+        const u32 notdone = __ballot_sync(mask, !done);
+        const u32 unknown = __ballot_sync(mask, c == NONE);  // chunk not in the ring
+        // run = lanes (in mask order) before the first not-retired one
+        u32 run = 0;
+        for (u32 m = mask; m; m &= m - 1) {
+            if ((notdone >> (__ffs(m) - 1)) & 1u) break;
+            ++run;
+        }
+        if (run == 0) return;
+        u32 last = mask;  // the run's last lane: its link is the new head
+        for (u32 r = 1; r < run; ++r) last &= last - 1;
+        const u32 ll = __ffs(last) - 1;
+        const u64 nh = shfl64(mask, nx, ll);
+        u32 won = 0;
+        if (lane == who) {
+            won = atomicCAS((u64*)&Q->vl_head, h, nh) == h ? 1u : 0u;
+            if (won) asm volatile("fence.sc.gpu;" ::: "memory");  // CAS before the next counter reads
+        }
+        if (!__shfl_sync(mask, won, who)) return;
+        const u32 part = __ballot_sync(mask, li < run);
+        arr_enqueue(v, v.q + Q->seg_src, mask, lane, part, c, true);
+        if (lane == who) atomicAdd((u64*)&Q->seg_live, (u64)-(i64)run);
+        // the run ended at a segment known not to be retired: its completer (or the
+        // advancer that reaches it) continues; a segment missing from the ring is
+        // looked at next round through the head link instead
+        if (run < L) {
+            u32 m = mask;
+            for (u32 r = 0; r < run; ++r) m &= m - 1;
+            if (!((unknown >> (__ffs(m) - 1)) & 1u)) return;
         }
     }
 }
@@ -581,9 +646,15 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
 __device__ __forceinline__ void vl_add(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
                                        bool part, u32 c, u32 cnt) {
     u32 done = 0;
-    if (part) done = (atomicAdd(vl_counter(v, c), cnt) + cnt == (u32)v.S_vl + 1u) ? 1u : 0u;
+    if (part) {
+        done = (atomicAdd(vl_counter(v, c), cnt) + cnt == (u32)v.S_vl + 1u) ? 1u : 0u;
+        if (done) asm volatile("fence.sc.gpu;" ::: "memory");  // counter before the head read
+    }
     const u32 dm = __ballot_sync(mask, done);
-    if (dm) vl_try_advance(v, Q, mask, lane, __ffs(dm) - 1);
+    if (dm) {
+        __syncwarp(mask);  // the completer's counter add before the other lanes' reads
+        vl_try_advance(v, Q, mask, lane, __ffs(dm) - 1);
+    }
 }
 __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
                                           u32 who, u64 s) {
@@ -750,6 +821,7 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
         const u64 key = part ? (u64)segc : (~0ull - lane);
         const u32 grp = __match_any_sync(mask, key);
         const u32 gl = __ffs(grp) - 1;
+        if (part && t % v.S_vl == 0) vl_extend_ring(v, Q, (u32)(t / v.S_vl));  // first slot of a segment
         vl_add(v, Q, mask, lane, part && lane == gl, segc, __popc(grp));
     }
     return got;

@@ -83,6 +83,8 @@ def _declare(L):
         "ouro_heap_last_error": (i32, [P, C.POINTER(u32), C.POINTER(u32), C.c_int]),
         "ouro_launch_alloc": (i32, [P, u64, u64, P, P, P]),
         "ouro_launch_alloc_u16": (i32, [P, u64, P, P, P]),
+        "ouro_heap_queue_links": (i32, [P, u32, C.POINTER(u64)]),
+        "ouro_heap_vl_ring": (i32, [P, u32, C.POINTER(u64)]),
         "ouro_launch_free": (i32, [P, u64, P, P]),
         "ouro_launch_write": (i32, [P, u64, P, u64, u32, P]),
         "ouro_launch_verify": (i32, [P, u64, P, u64, u32, P, P]),
@@ -309,6 +311,18 @@ class Heap:
     def set_checks(self, on: bool = True):
         """Debug mode: verify queue/bitmap invariants on every device op."""
         check(lib().ouro_heap_set_checks(self._h, int(on)), "set_checks")
+
+    def queue_links(self, qi: int):
+        """Debug: (count, head ticket, vl_head, vl_tail) of queue qi."""
+        out = (C.c_uint64 * 4)()
+        check(lib().ouro_heap_queue_links(self._h, qi, out), "queue_links")
+        return tuple(out)
+
+    def vl_ring(self, qi: int):
+        """Debug: the dequeue-side VirtualList ring of queue qi (256 links)."""
+        out = (C.c_uint64 * 256)()
+        check(lib().ouro_heap_vl_ring(self._h, qi, out), "vl_ring")
+        return list(out)
 
     def reset(self, stream=None):
         check(lib().ouro_heap_reset(self._h, _stream(stream)), "reset")

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 #include <vector>
@@ -570,6 +571,8 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
         q.count = 0; q.head = 0; q.tail = 0; q.seg_live = 0; q.seg_hwm = 0;
         q.vl_head = q.vl_tail = ((u64)0 << 32) | NONE;
         for (auto& r : q.vl_recent) r = NONE_LINK;
+        for (auto& r : q.vl_deq) r = NONE_LINK;
+        q.vl_front = 0;
     }
     auto ring_fill = [&](ouro_queue_dev& q, u64 cap, int mode, u32 first, u32 ppc) -> ouro_status {
         const u64 R = q.ring_mask + 1;
@@ -625,6 +628,9 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
                 q.vl_tail = ((u64)(m - 1) << 32) | (seg0 + m - 1);
                 for (u32 i = m > OURO_VL_RECENT ? m - OURO_VL_RECENT : 0; i < m; ++i)
                     q.vl_recent[i % OURO_VL_RECENT] = ((u64)i << 32) | (seg0 + i);
+                for (u32 i = 0; i < std::min<u32>(m, OURO_VL_RECENT); ++i)
+                    q.vl_deq[i] = ((u64)i << 32) | (seg0 + i);
+                q.vl_front = std::min<u32>(m, OURO_VL_RECENT) - 1;
             }
             // private segment pool: reserve chunks not used by the prefill
             std::vector<u64> ps(P.ring_mask + 1, 0);
@@ -946,6 +952,26 @@ ouro_status ouro_heap_digest(ouro_heap* H, ouro_digest* out, void* stream) {
     CK(cudaSetDevice(H->device));
     CK(cudaStreamSynchronize(S(stream)));
     return compute_digest(H, out, nullptr, nullptr, S(stream));
+}
+
+ouro_status ouro_heap_queue_links(ouro_heap* H, uint32_t qi, uint64_t out[4]) {
+    if (!H || !out || qi >= H->nq) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    CK(cudaDeviceSynchronize());
+    const ouro_queue_dev* q = H->d_q + qi;
+    CK(cudaMemcpy(&out[0], &q->count, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&out[1], &q->head, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&out[2], &q->vl_head, 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&out[3], &q->vl_tail, 8, cudaMemcpyDeviceToHost));
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_vl_ring(ouro_heap* H, uint32_t qi, uint64_t out[OURO_VL_RECENT]) {
+    if (!H || !out || qi >= H->nq) return OURO_ERR_USAGE;
+    CK(cudaSetDevice(H->device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out, &(H->d_q + qi)->vl_deq[0], 8 * OURO_VL_RECENT, cudaMemcpyDeviceToHost));
+    return OURO_OK;
 }
 
 ouro_status ouro_heap_stats(ouro_heap* H, ouro_stats* out, void* stream) {
