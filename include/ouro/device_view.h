@@ -104,6 +104,9 @@ typedef struct ouro_heap_view {
      * n_0 = pq_n0, n_k = pq_q for k > 0, so decode is arithmetic, not a load. */
     uint32_t pq_n0, pq_q;
     uint32_t pq_s[32];
+    /* latest queue observation per (SM, queue tag): 256 x 32 u64 hints (see
+     * ouro_device.cuh sm_hint_row); hints only, never a retry round's observation */
+    ouro_u64* sm_hint;
 } ouro_heap_view;
 
 #endif

@@ -188,23 +188,56 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 // the first round: after its failed try), so OutOfMemory is declared only
 // after max_retries distinct observations of "no page obtainable"
 // -- a queue that refills while a warp retries is seen by its next round.
-// Entry: [63:8] poll issue time / 256 ns, [7:3] queue tag, [2] no result yet,
-// [1] in flight, [0] empty.  Shared memory is not initialised for kernels that
-// do not call ouro_block_init, so an entry counts only if its time lies in
+// "Issued after" is a per-(block, queue) poll sequence number, not a clock:
+// polls of one entry are issued one at a time and each only after the
+// previous one completed, so a higher sequence number was issued later.  (An
+// ordering by %globaltimer ticks made every round wait for the next tick:
+// ~1 us per round, 372 us per OOM-storm launch.)
+// Poll entry: [63:32] issue time (globaltimer / 256 ns), [31:8] sequence,
+// [7:3] queue tag, [1] in flight, [0] empty.  Hint entry (first-try hints and
+// pre-checks only, never a round's observation): [63:32] time, [7:3] tag,
+// [0] empty.  Shared memory is not initialised for kernels that do not call
+// ouro_block_init, so an entry counts only if its time lies in
 // [now - window, now + kPollSkew]: garbage that looks like a future entry is
 // rejected.
-constexpr u64 kPollWindow = 32;  // x 256 ns = 8.2 us
-constexpr u64 kPollSkew = 2;     // entries written just after we read the clock
-__device__ __forceinline__ bool poll_recent(u64 now, u64 e, u64 window) {
-    return now - (e >> 8) + kPollSkew < window + kPollSkew;
-}
-__device__ __forceinline__ u64 gtime256() {
+constexpr u32 kPollWindow = 32;  // x 256 ns = 8.2 us
+constexpr u32 kPollSkew = 2;     // entries written just after we read the clock
+constexpr u32 kSeqMask = 0xFFFFFFu;
+__device__ __forceinline__ u32 gtime32() {
     u64 t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t >> 8;
+    return (u32)(t >> 8);
+}
+__device__ __forceinline__ bool time_recent(u32 now, u64 e, u32 window) {
+    return now - (u32)(e >> 32) + kPollSkew < window + kPollSkew;
+}
+__device__ __forceinline__ u32 e_seq(u64 e) { return (u32)(e >> 8) & kSeqMask; }
+__device__ __forceinline__ bool seq_after(u32 a, u32 b) { return ((a - b) & kSeqMask) - 1u < (kSeqMask >> 1); }
+__device__ __forceinline__ u64 mk_entry(u32 now, u32 seq, u64 tag, u32 flags) {
+    return ((u64)now << 32) | ((u64)(seq & kSeqMask) << 8) | (tag << 3) | flags;
+}
+#ifdef OURO_ROUND_TRACE
+// Experiment builds only: per-SM accumulators of where a retry round's time goes.
+// [0] poller count-load cycles [1] polls [2] poll_after cycles [3] poll_after calls
+// [4] round cycles [5] rounds [6] poll_after loop iterations [7] backoff cycles
+__device__ unsigned long long ouro_trace[256 * 8];
+__device__ __forceinline__ void trace_add(u32 i, u64 x) { atomicAdd(&ouro_trace[(sm_id() & 255) * 8 + i], x); }
+#define OURO_TR(stmt) stmt
+#else
+#define OURO_TR(stmt)
+#endif
+constexpr u32 kPollEntries = 16;
+// How a warp waiting for this block's in-flight poll idles between checks.
+#ifndef OURO_POLL_WAIT_NS
+#define OURO_POLL_WAIT_NS 32
+#endif
+__device__ __forceinline__ void poll_wait() {
+#if OURO_POLL_WAIT_NS >= 0
+    __nanosleep(OURO_POLL_WAIT_NS);
+#endif
 }
 __device__ __forceinline__ u64* poll_cache() {
-    __shared__ u64 cache[16];
+    __shared__ u64 cache[2 * kPollEntries];  // [0,16) polls, [16,32) hints
     return cache;
 }
 // Queue structs are laid out consecutively, so the struct index is a collision-free
@@ -213,65 +246,98 @@ __device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) {
     return ((u64)Q / sizeof(ouro_queue_dev)) & 31u;
 }
 __device__ __forceinline__ u64* poll_slot(u64 tag) { return poll_cache() + (tag & 15); }
+__device__ __forceinline__ u64* hint_slot(u64 tag) { return poll_cache() + kPollEntries + (tag & 15); }
+__device__ __forceinline__ bool tag_is(u64 e, u64 tag) { return ((e >> 3) & 31u) == tag; }
 
-// An observation of (count - floor <= 0) issued strictly after tick `after`;
-// *when receives its issue tick.  Reuses a completed poll of this block, waits
-// for one in flight, or issues one.
-static __device__ __noinline__ bool poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u64* slot, u64 after,
-                                               u64* when) {
+// Per-SM hints in HBM (v.sm_hint: 32 entries per SM, hint format): the latest
+// observation any block on this SM made of each queue.  ouro_block_init(v)
+// seeds a fresh block's hints from them, so the blocks of an OOM storm that
+// start after the queue ran dry make their first try a block-combined poll
+// (one count load per block) instead of an RMW + undo pair per warp.
+__device__ __forceinline__ u64* sm_hint_row(const ouro_heap_view& v) {
+    return v.sm_hint ? v.sm_hint + (u64)(sm_id() & 255u) * 32u : nullptr;
+}
+__device__ __forceinline__ void publish_hint(u64* smh, u64 tag, u64 h) {
+    *reinterpret_cast<volatile u64*>(hint_slot(tag)) = h;
+    if (smh) st_rlx(smh + tag, h);
+}
+
+// The sequence a warp must exceed with its next observation: whatever this
+// block's entry holds now (completed or in flight -- an in-flight poll may have
+// been issued before the caller's failed try).
+__device__ __forceinline__ u32 poll_seq_now(u64 tag) {
+    return e_seq(*reinterpret_cast<volatile u64*>(poll_slot(tag)));
+}
+
+// An observation of (count - floor <= 0) with sequence after `after`.
+// Returns (sequence << 1) | empty -- by value: a result pointer into this
+// __noinline__ function would put the caller's round state in local memory,
+// one L2 write per round.  Reuses a completed poll of this block, waits for
+// one in flight, or issues one.
+__device__ __forceinline__ u32 obs_seq(u32 o) { return o >> 1; }
+__device__ __forceinline__ bool obs_empty(u32 o) { return (o & 1u) != 0; }
+static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
+    u64* slot = poll_slot(tag);
+    OURO_TR(const u64 c0 = clock64(); trace_add(3, 1));
     for (int spins = 0; spins < 4096; ++spins) {
-        const u64 now = gtime256();
+        OURO_TR(trace_add(6, 1));
+        const u32 now = gtime32();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
-        const bool mine_tag = ((e >> 3) & 31u) == tag && poll_recent(now, e, 4 * kPollWindow);
-        const u64 t = e >> 8;
-        if (mine_tag && (i64)(t - after) > 0) {
-            if (!(e & 6u)) { *when = t; return (e & 1u) != 0; }  // completed, issued after `after`
-            if (e & 2u) { __nanosleep(32); continue; }            // in flight, issued after: wait
+        const bool mine = tag_is(e, tag) && time_recent(now, e, 4 * kPollWindow);
+        if (mine && (e & 2u)) { poll_wait(); continue; }  // in flight: its result or a newer poll
+        if (mine && seq_after(e_seq(e), after)) {
+            OURO_TR(trace_add(2, clock64() - c0));
+            return (e_seq(e) << 1) | (u32)(e & 1u);
         }
-        if (mine_tag && (e & 2u)) { __nanosleep(32); continue; }  // an older poll in flight
-        if ((i64)(now - after) <= 0) { __nanosleep(64); continue; }  // our poll must start later
-        const u64 keep = mine_tag ? (e & 5u) : 4u;  // old result stays as a hint
-        if (atomicCAS(slot, e, (now << 8) | (tag << 3) | 2u | keep) != e) continue;
-        const bool empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
-        atomicExch(slot, (now << 8) | (tag << 3) | (empty ? 1u : 0u));
-        *when = now;
-        return empty;
+        const u32 ns = (after + 1u) & kSeqMask;
+        const u64 fl = mk_entry(now, ns, tag, 2u);
+        if (atomicCAS(slot, e, fl) != e) continue;
+        OURO_TR(const u64 c1 = clock64());
+        const u32 empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
+
+        atomicCAS(slot, fl, mk_entry(now, ns, tag, empty));  // unless a stale-entry reset replaced it
+        publish_hint(smh, tag, mk_entry(now, 0, tag, empty));
+        OURO_TR(trace_add(0, clock64() - c1); trace_add(1, 1); trace_add(2, clock64() - c0));
+        return (ns << 1) | empty;
     }
-    const u64 now = gtime256();
-    *when = now;
-    return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0;
+    return (((after + 1u) & kSeqMask) << 1) | ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u);
 }
 
 // Pre-check before a reservation RMW (hint: the RMW decides).  One LDS, one
 // clock read when this block has a recent completed observation.
-__device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor) {
+__device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64* smh) {
     const u64 tag = poll_tag(Q);
-    u64* slot = poll_slot(tag);
-    const u64 e = *reinterpret_cast<volatile u64*>(slot);
-    const u64 now = gtime256();
-    if (((e ^ (tag << 3)) & 0xFCu) == 0u && poll_recent(now, e, kPollWindow)) return (e & 1u) != 0;
-    u64 w;
-    return poll_after(Q, floor, tag, slot, now - kPollWindow, &w);
+    const u64 h = *reinterpret_cast<volatile u64*>(hint_slot(tag));
+    if (tag_is(h, tag) && time_recent(gtime32(), h, kPollWindow)) return (h & 1u) != 0;
+    return obs_empty(poll_after(Q, floor, tag, poll_seq_now(tag), smh));
 }
 
 // Failed retry rounds on a group leader: backoff, then a
 // block-combined observation of the class queue (and, for the chunk kind, of
-// the pool) issued after the previous round's; stops when one sees work
+// the pool) newer than the previous round's; stops when one sees work
 // (returns false) or when the budget is spent (returns true: OutOfMemory).
 // *attempt counts rounds as the oracle does.
 __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
                                             i64 pfloor, u32* attempt) {
     u32 a = *attempt;
     const u32 maxr = v.max_retries;
+    u64* smh = sm_hint_row(v);
     const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
-    u64* sq = poll_slot(tq);
-    u64* sp = poll_slot(tp);
-    u64 lq = gtime256(), lp = lq;  // the failed try happened before this tick
+    u32 lq = poll_seq_now(tq), lp = P ? poll_seq_now(tp) : 0;  // read after the failed try returned
     for (;;) {
         if (++a >= maxr) { *attempt = a; return true; }
+        OURO_TR(const u64 r0 = clock64());
         backoff(v, a);
-        if (!poll_after(Q, 0, tq, sq, lq, &lq)) break;
-        if (P && !poll_after(P, pfloor, tp, sp, lp, &lp)) break;
+        OURO_TR(trace_add(7, clock64() - r0));
+        const u32 oq = poll_after(Q, 0, tq, lq, smh);
+        OURO_TR(trace_add(4, clock64() - r0); trace_add(5, 1));
+        lq = obs_seq(oq);
+        if (!obs_empty(oq)) break;
+        if (P) {
+            const u32 op = poll_after(P, pfloor, tp, lp, smh);
+            lp = obs_seq(op);
+            if (!obs_empty(op)) break;
+        }
     }
     *attempt = a;
     return false;
@@ -281,44 +347,43 @@ __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_
 // first try's RMW into load-then-RMW, which reserves exactly the same.)
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
-    const u64 e = *reinterpret_cast<volatile u64*>(poll_slot(tag));
-    return ((e ^ (tag << 3)) & 0xFDu) == 1u && poll_recent(gtime256(), e, 4 * kPollWindow);
+    const u64 e = *reinterpret_cast<volatile u64*>(hint_slot(tag));
+    return tag_is(e, tag) && (e & 1u) && time_recent(gtime32(), e, 4 * kPollWindow);
 }
-// A reservation RMW issued after tick t0 found the queue empty: record it as an
-// observation issued at t0 (never later than the RMW itself).
-__device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u64 t0) {
+// A reservation RMW issued at tick t0 found the queue empty: record the hint.
+__device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u32 t0, u64* smh) {
     const u64 tag = poll_tag(Q);
-    u64* slot = poll_slot(tag);
-    const u64 e = *reinterpret_cast<volatile u64*>(slot);
-    if ((e & 2u) && ((e >> 3) & 31u) == tag) return;  // a poll is in flight: leave it
-    if (((e >> 3) & 31u) == tag && !(e & 4u) && (i64)((e >> 8) - t0) >= 0) return;  // newer already
-    atomicCAS(slot, e, (t0 << 8) | (tag << 3) | 1u);
+    publish_hint(smh, tag, mk_entry(t0, 0, tag, 1u));
 }
 
 // Count reservation (broker-queue style).
 // `precheck`: read the count first and skip the RMW when it is already empty
 // (retries and chunk-queue probes); the reservation result is the same either way.
 // `combine`: take the pre-check from the block's poll combiner (retry rounds).
-// Without precheck the first try goes straight to the RMW unless this block saw
-// the queue empty lately (then load first: an OOM storm costs loads, not RMW pairs).
-__device__ __forceinline__ u32 reserve_deq(ouro_queue_dev* Q, u32 n, i64 floor, bool precheck = true,
-                                           bool combine = false) {
+// Without precheck the first try goes straight to the RMW unless this block (or,
+// through the seeded hints, its SM) saw the queue empty lately: then the try
+// starts with a block-combined observation issued after the call began (an OOM
+// storm costs one count load per block, not an RMW + undo pair per warp); a
+// non-empty answer still goes through the RMW, which decides.
+__device__ __forceinline__ u32 reserve_deq(const ouro_heap_view& v, ouro_queue_dev* Q, u32 n, i64 floor,
+                                           bool precheck = true, bool combine = false) {
     if (precheck) {
         if (combine) {
-            if (observed_empty(Q, floor)) return 0;
+            if (observed_empty(Q, floor, sm_hint_row(v))) return 0;
         } else if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
             return 0;
         }
-    } else if (hint_empty(Q) && (i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
-        return 0;
+    } else if (hint_empty(Q)) {
+        const u64 tag = poll_tag(Q);
+        if (obs_empty(poll_after(Q, floor, tag, poll_seq_now(tag), sm_hint_row(v)))) return 0;
     }
-    const u64 t0 = gtime256();
+    const u32 t0 = gtime32();
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
     if (got < n) {
         atomicAdd((u64*)&Q->count, (u64)(n - got));
-        note_empty(Q, t0);
+        note_empty(Q, t0, sm_hint_row(v));
     }
     return got;
 }
@@ -395,7 +460,7 @@ __device__ __forceinline__ u32 arr_dequeue(const ouro_heap_view& v, ouro_queue_d
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor, precheck, combine);
+        got = reserve_deq(v, Q, n, floor, precheck, combine);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -513,9 +578,14 @@ __device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_de
             bool ok = true;
             while (i != (u32)s) {
                 const u64 nx = ld_rlx(chunk_words(v, cur));
-                // the link read is valid iff segment i was not retired before it:
-                // retirement moves the head past i first, so re-check the head's seq
-                if ((int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0 || nx == NONE_LINK) { ok = false; break; }
+                // The link read is valid iff it names segment i + 1: a link word only
+                // ever holds the link to its own segment's successor, and a recycled
+                // chunk serves a newer segment (higher seq) or is being zeroed.  The
+                // head re-check just stops walks that fell behind.
+                if (nx == NONE_LINK || lseq(nx) != i + 1u || (int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0) {
+                    ok = false;
+                    break;
+                }
                 cur = lchk(nx);
                 ++i;
                 if (!from_tail) st_rlx(&Q->vl_deq[i % OURO_VL_RECENT], nx);  // record the hop
@@ -565,7 +635,7 @@ __device__ __forceinline__ void vl_extend_ring(const ouro_heap_view& v, ouro_que
     }
     while (i != T) {
         const u64 nx = ld_rlx(chunk_words(v, cur));
-        if (nx == NONE_LINK || (int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0) break;
+        if (nx == NONE_LINK || lseq(nx) != i + 1u || (int)(lseq(ld_rlx(&Q->vl_head)) - i) > 0) break;
         cur = lchk(nx);
         ++i;
         st_rlx(&Q->vl_deq[i % OURO_VL_RECENT], nx);
@@ -583,12 +653,16 @@ __device__ __forceinline__ void vl_extend_ring(const ouro_heap_view& v, ouro_que
 // one warp enqueue (in segment order).  Only the CAS winner continues; a loser
 // stops.  A segment c completed while the head was behind it is not lost: its
 // completer increments c's counter, fences, then reads the head (vl_add); the
-// advancer CASes the head, fences, then reads the counters -- with both fences
-// seq-cst, at least one sees the other's write (store-buffering litmus).
+// advancer CASes the head, fences, then reads the new head segment's counter
+// again (the next loop iteration) -- with both fences seq-cst, at least one
+// sees the other's write (store-buffering litmus).  The winner must re-read:
+// counters it read BEFORE its CAS may predate a completer that then saw the old
+// head and lost its own CAS to ours (that lost wakeup stalled the head and
+// starved segment creation under 2^20-thread VLPQ loads).
 __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
                                                u32 lane, u32 who) {
     const u32 full = (u32)v.S_vl + 1u;
-    const u32 L = __popc(mask), li = __popc(mask & lanemask_lt());
+    const u32 li = __popc(mask & lanemask_lt());
     for (;;) {
         u64 h = 0;
         if (lane == who) h = ld_rlx(&Q->vl_head);
@@ -609,7 +683,6 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
             done = nx != NONE_LINK && lseq(nx) == seq + 1u;
         }
         const u32 notdone = __ballot_sync(mask, !done);
-        const u32 unknown = __ballot_sync(mask, c == NONE);  // chunk not in the ring
         // run = lanes (in mask order) before the first not-retired one
         u32 run = 0;
         for (u32 m = mask; m; m &= m - 1) {
@@ -622,22 +695,12 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
         const u32 ll = __ffs(last) - 1;
         const u64 nh = shfl64(mask, nx, ll);
         u32 won = 0;
-        if (lane == who) {
-            won = atomicCAS((u64*)&Q->vl_head, h, nh) == h ? 1u : 0u;
-            if (won) asm volatile("fence.sc.gpu;" ::: "memory");  // CAS before the next counter reads
-        }
+        if (lane == who) won = atomicCAS((u64*)&Q->vl_head, h, nh) == h ? 1u : 0u;
         if (!__shfl_sync(mask, won, who)) return;
+        asm volatile("fence.sc.gpu;" ::: "memory");  // our CAS before every lane's next counter reads
         const u32 part = __ballot_sync(mask, li < run);
         arr_enqueue(v, v.q + Q->seg_src, mask, lane, part, c, true);
         if (lane == who) atomicAdd((u64*)&Q->seg_live, (u64)-(i64)run);
-        // the run ended at a segment known not to be retired: its completer (or the
-        // advancer that reaches it) continues; a segment missing from the ring is
-        // looked at next round through the head link instead
-        if (run < L) {
-            u32 m = mask;
-            for (u32 r = 0; r < run; ++r) m &= m - 1;
-            if (!((unknown >> (__ffs(m) - 1)) & 1u)) return;
-        }
     }
 }
 // Warp-collective: lanes in `part` add `cnt` to segment `c`'s retire counter
@@ -646,13 +709,11 @@ __device__ __forceinline__ void vl_try_advance(const ouro_heap_view& v, ouro_que
 __device__ __forceinline__ void vl_add(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
                                        bool part, u32 c, u32 cnt) {
     u32 done = 0;
-    if (part) {
-        done = (atomicAdd(vl_counter(v, c), cnt) + cnt == (u32)v.S_vl + 1u) ? 1u : 0u;
-        if (done) asm volatile("fence.sc.gpu;" ::: "memory");  // counter before the head read
-    }
+    if (part) done = (atomicAdd(vl_counter(v, c), cnt) + cnt == (u32)v.S_vl + 1u) ? 1u : 0u;
     const u32 dm = __ballot_sync(mask, done);
     if (dm) {
-        __syncwarp(mask);  // the completer's counter add before the other lanes' reads
+        // every lane: the completers' counter adds before any lane's head / counter reads
+        asm volatile("fence.sc.gpu;" ::: "memory");
         vl_try_advance(v, Q, mask, lane, __ffs(dm) - 1);
     }
 }
@@ -779,7 +840,7 @@ __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 ma
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(Q, n, floor, precheck, combine);
+        got = reserve_deq(v, Q, n, floor, precheck, combine);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -1247,7 +1308,33 @@ __device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, 
 // kernel left in shared memory.  The C-ABI launchers call it.
 __device__ __forceinline__ void ouro_block_init() {
     const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-    if (t < 16) ouro_dev::poll_cache()[t] = 0;
+    const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
+    for (unsigned i = t; i < 2 * ouro_dev::kPollEntries; i += nt) ouro_dev::poll_cache()[i] = 0;
+    __syncthreads();
+}
+// Same, and seed the block's hints from the latest observations other blocks on
+// this SM published for heap `h` (one L2 load per hint entry, at block start).
+__device__ __forceinline__ void ouro_block_init(const ouro_heap_view& h) {
+    using namespace ouro_dev;
+    const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
+    u64* cache = poll_cache();
+    for (unsigned i = t; i < 2 * kPollEntries; i += nt) cache[i] = 0;
+    __syncthreads();
+    const u64* row = sm_hint_row(h);
+    if (row) {
+        // Chunk kind: only the pool's hint.  A chunk class queue is empty whenever
+        // its few entries are in transit, so a seeded "empty" would
+        // send served requests to the pool with an older observation.
+        const u64 pool_tag = poll_tag(h.q + h.K);
+        const u32 now = gtime32();
+        for (unsigned i = t; i < 32; i += nt) {
+            if (h.kind == KIND_CHUNK && i != pool_tag) continue;
+            const u64 e = ld_rlx(row + i);
+            // entry of queue tag i, recent: may go to the hint slot (tags i and i+16 share one)
+            if (tag_is(e, i) && time_recent(now, e, 4 * kPollWindow)) cache[kPollEntries + (i & 15)] = e;
+        }
+    }
     __syncthreads();
 }
 

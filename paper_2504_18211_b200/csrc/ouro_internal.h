@@ -32,6 +32,7 @@ struct ouro_heap {
     ouro_queue_dev* d_q = nullptr;
     ouro_u64* d_ctr = nullptr;
     uint32_t* d_sticky = nullptr;
+    ouro_u64* d_sm_hint = nullptr;  // per-SM queue hints (256 x 32)
     uint32_t* d_pq = nullptr;      // page kind partition: start[K], n[K], s[K]
     uint8_t* d_touched = nullptr;  // churn reuse bitmap (lazy)
     std::vector<void*> owned;      // slot rings, dirs, dcnts

@@ -40,6 +40,7 @@ using ouro_host::Geometry;
 namespace {
 
 constexpr int kBlock = 256;
+constexpr size_t kSmHintBytes = 256 * 32 * 8;
 // Launch shape of the malloc/free/churn drivers (one request per thread, requests
 // independent).  g_op_waves = 0: one thread per request (grid = n / block);
 // g_op_waves = w >= 1: persistent grid of w x (resident CTAs per SM) x SMs that
@@ -128,9 +129,15 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 // ------------------------------------------------------------ driver phases ----
 // (Forcing 32 registers for 8 blocks/SM was measured slower: the spills cost
 // more than the extra warps gain, profiles/r1_ncu_summary.md.)
+// 6 resident blocks per SM (<= 40 registers): the blocks of an OOM storm only
+// wait out their retry rounds, so residency sets how many waves the storm takes
+// (pq1g 8 KiB alloc 297 -> 276 us, cq1g 595 -> 496 us; served sizes unchanged).
+#ifndef OURO_ALLOC_MIN_BLOCKS
+#define OURO_ALLOC_MIN_BLOCKS 6
+#endif
 template <int KIND, int FL, class SZ = u32>
-__global__ void __launch_bounds__(kBlock) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const SZ* sizes, void** out) {
-    ouro_block_init();
+__global__ void __launch_bounds__(kBlock, OURO_ALLOC_MIN_BLOCKS) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const SZ* sizes, void** out) {
+    ouro_block_init(v);
     const u64 stride = (u64)gridDim.x * blockDim.x;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
         const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
@@ -283,7 +290,7 @@ __device__ __forceinline__ void churn_slot(const ouro_heap_view& v, u64 t, bool 
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
                                                   uint8_t* touched, u64* res) {
-    ouro_block_init();
+    ouro_block_init(v);
     const u64 stride = (u64)gridDim.x * blockDim.x;
     for (u64 t = blockIdx.x * (u64)blockDim.x + threadIdx.x; t - threadIdx.x % 32 < n; t += stride)
         churn_slot<KIND, FL>(v, t, t < n, r, seed, slots, touched, res);
@@ -566,6 +573,7 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
     CK(cudaMemsetAsync(H->d_assigned, 0, (size_t)K * 4, st));
     CK(cudaMemsetAsync(H->d_ctr, 0, (size_t)OURO_CTR_SHARDS * (2 * K + OURO_CTR_N) * 8, st));
     CK(cudaMemsetAsync(H->d_sticky, 0, 8, st));
+    CK(cudaMemsetAsync(H->d_sm_hint, 0, kSmHintBytes, st));
     if (H->d_touched) CK(cudaMemsetAsync(H->d_touched, 0, g.heap / g.minp / 8 + 8, st));
     for (auto& q : H->hq) {
         q.count = 0; q.head = 0; q.tail = 0; q.seg_live = 0; q.seg_hwm = 0;
@@ -665,6 +673,7 @@ void make_view(ouro_heap* H) {
     v.q = H->d_q;
     v.ctr = H->d_ctr;
     v.sticky = H->d_sticky;
+    v.sm_hint = H->d_sm_hint;
     v.heap_bytes = g.heap;
     v.chunk_bytes = g.chunk;
     v.S_va = g.chunk / 8;
@@ -813,8 +822,16 @@ ouro_status compute_digest(ouro_heap* H, ouro_digest* out, DigestDev* hd_out, st
     cudaFree(where);
     cudaFree(entries);
     bool ok = hd.bad == 0 && !host_bad;
+    const bool dbg = std::getenv("OURO_DIGEST_DEBUG") != nullptr;
+    if (dbg && !ok) std::fprintf(stderr, "digest: dev bad %u host_bad %d\n", (unsigned)hd.bad, (int)host_bad);
+    int shown = 0;
     for (u32 c = 0; c < N; ++c) {
-        if (hw[c] + host_where_add[c] != 1) ok = false;
+        if (hw[c] + host_where_add[c] != 1) {
+            ok = false;
+            if (dbg && shown++ < 16)
+                std::fprintf(stderr, "digest: chunk %u where %u segments %u meta %016llx\n", c, hw[c],
+                             host_where_add[c], (unsigned long long)meta[c]);
+        }
         if (H->cfg.allocator_kind == OURO_KIND_CHUNK) {
             const u32 s8 = (u32)(meta[c] >> 32) & 0xFF;
             const bool has_free = s8 >= 1 && s8 <= K && (u32)meta[c] > 0;
@@ -863,7 +880,9 @@ ouro_status ouro_heap_create(const ouro_config* cfg, int device, ouro_heap** out
     H->d_assigned = static_cast<u32*>(dalloc(H, (size_t)g.K * 4));
     H->d_ctr = static_cast<u64*>(dalloc(H, (size_t)OURO_CTR_SHARDS * (2 * g.K + OURO_CTR_N) * 8));
     H->d_sticky = static_cast<u32*>(dalloc(H, 8));
-    if (!H->d_heap || !H->d_meta || !H->d_bitmap || !H->d_assigned || !H->d_ctr || !H->d_sticky) return fail(OURO_ERR_CUDA);
+    H->d_sm_hint = static_cast<u64*>(dalloc(H, kSmHintBytes));
+    if (!H->d_heap || !H->d_meta || !H->d_bitmap || !H->d_assigned || !H->d_ctr || !H->d_sticky || !H->d_sm_hint)
+        return fail(OURO_ERR_CUDA);
     if (plan(H) != OURO_OK) return fail(OURO_ERR_CUDA);
     H->d_q = static_cast<ouro_queue_dev*>(dalloc(H, H->nq * sizeof(ouro_queue_dev)));
     if (!H->d_q) return fail(OURO_ERR_CUDA);
@@ -1212,6 +1231,16 @@ ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial
     return OURO_OK;
 }
 
+#ifdef OURO_ROUND_TRACE
+extern "C" ouro_status ouro_debug_trace(unsigned long long* out8, int reset) {
+    static unsigned long long h[256 * 8];
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpyFromSymbol(h, ouro_dev::ouro_trace, sizeof(h)));
+    for (int i = 0; i < 8; ++i) { out8[i] = 0; for (int s = 0; s < 256; ++s) out8[i] += h[s * 8 + i]; }
+    if (reset) { std::memset(h, 0, sizeof(h)); CK(cudaMemcpyToSymbol(ouro_dev::ouro_trace, h, sizeof(h))); }
+    return OURO_OK;
+}
+#endif
 ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     if (!ops_per_s) return OURO_ERR_USAGE;
     CK(cudaSetDevice(device));
