@@ -216,16 +216,6 @@ __device__ __forceinline__ bool seq_after(u32 a, u32 b) { return ((a - b) & kSeq
 __device__ __forceinline__ u64 mk_entry(u32 now, u32 seq, u64 tag, u32 flags) {
     return ((u64)now << 32) | ((u64)(seq & kSeqMask) << 8) | (tag << 3) | flags;
 }
-#ifdef OURO_ROUND_TRACE
-// Experiment builds only: per-SM accumulators of where a retry round's time goes.
-// [0] poller count-load cycles [1] polls [2] poll_after cycles [3] poll_after calls
-// [4] round cycles [5] rounds [6] poll_after loop iterations [7] backoff cycles
-__device__ unsigned long long ouro_trace[256 * 8];
-__device__ __forceinline__ void trace_add(u32 i, u64 x) { atomicAdd(&ouro_trace[(sm_id() & 255) * 8 + i], x); }
-#define OURO_TR(stmt) stmt
-#else
-#define OURO_TR(stmt)
-#endif
 constexpr u32 kPollEntries = 16;
 // How a warp waiting for this block's in-flight poll idles between checks.
 #ifndef OURO_POLL_WAIT_NS
@@ -278,26 +268,21 @@ __device__ __forceinline__ u32 obs_seq(u32 o) { return o >> 1; }
 __device__ __forceinline__ bool obs_empty(u32 o) { return (o & 1u) != 0; }
 static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
     u64* slot = poll_slot(tag);
-    OURO_TR(const u64 c0 = clock64(); trace_add(3, 1));
     for (int spins = 0; spins < 4096; ++spins) {
-        OURO_TR(trace_add(6, 1));
         const u32 now = gtime32();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
         const bool mine = tag_is(e, tag) && time_recent(now, e, 4 * kPollWindow);
         if (mine && (e & 2u)) { poll_wait(); continue; }  // in flight: its result or a newer poll
         if (mine && seq_after(e_seq(e), after)) {
-            OURO_TR(trace_add(2, clock64() - c0));
             return (e_seq(e) << 1) | (u32)(e & 1u);
         }
         const u32 ns = (after + 1u) & kSeqMask;
         const u64 fl = mk_entry(now, ns, tag, 2u);
         if (atomicCAS(slot, e, fl) != e) continue;
-        OURO_TR(const u64 c1 = clock64());
         const u32 empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
 
         atomicCAS(slot, fl, mk_entry(now, ns, tag, empty));  // unless a stale-entry reset replaced it
         publish_hint(smh, tag, mk_entry(now, 0, tag, empty));
-        OURO_TR(trace_add(0, clock64() - c1); trace_add(1, 1); trace_add(2, clock64() - c0));
         return (ns << 1) | empty;
     }
     return (((after + 1u) & kSeqMask) << 1) | ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u);
@@ -326,11 +311,8 @@ __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_
     u32 lq = poll_seq_now(tq), lp = P ? poll_seq_now(tp) : 0;  // read after the failed try returned
     for (;;) {
         if (++a >= maxr) { *attempt = a; return true; }
-        OURO_TR(const u64 r0 = clock64());
         backoff(v, a);
-        OURO_TR(trace_add(7, clock64() - r0));
         const u32 oq = poll_after(Q, 0, tq, lq, smh);
-        OURO_TR(trace_add(4, clock64() - r0); trace_add(5, 1));
         lq = obs_seq(oq);
         if (!obs_empty(oq)) break;
         if (P) {

@@ -1231,16 +1231,6 @@ ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial
     return OURO_OK;
 }
 
-#ifdef OURO_ROUND_TRACE
-extern "C" ouro_status ouro_debug_trace(unsigned long long* out8, int reset) {
-    static unsigned long long h[256 * 8];
-    CK(cudaDeviceSynchronize());
-    CK(cudaMemcpyFromSymbol(h, ouro_dev::ouro_trace, sizeof(h)));
-    for (int i = 0; i < 8; ++i) { out8[i] = 0; for (int s = 0; s < 256; ++s) out8[i] += h[s * 8 + i]; }
-    if (reset) { std::memset(h, 0, sizeof(h)); CK(cudaMemcpyToSymbol(ouro_dev::ouro_trace, h, sizeof(h))); }
-    return OURO_OK;
-}
-#endif
 ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     if (!ops_per_s) return OURO_ERR_USAGE;
     CK(cudaSetDevice(device));

@@ -313,3 +313,27 @@ def test_no_spurious_oom_while_queue_refills(cuda, flavor):
             h.launch_free(n, ptrs)
             torch.cuda.synchronize()
             assert h.last_error()[0] == 0
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_virtual_list_retirement_under_load(cuda, kind):
+    """Regression: VirtualList segment retirement at 2^20 threads (8 GiB heap,
+    8190-slot segments, ~128 segments retired and created per phase).  A head
+    advance whose CAS won could miss a segment completed concurrently by a warp
+    that saw the old head and lost its own CAS; the head then stalled, segment
+    creation starved (TimeoutError) and the free-all partition broke in about a
+    third of the runs.  Six alloc/free rounds, canonical digest after each."""
+    torch = cuda
+    n = 1 << 20
+    with ob.Heap(_hc(kind, 2, 8 << 30)) as h:
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        for rep in range(6):
+            size = 16 if rep % 2 == 0 else 512
+            h.launch_alloc(n, ptrs, size=size)
+            torch.cuda.synchronize()
+            assert int((ptrs != 0).sum()) == n, rep
+            h.launch_free(n, ptrs)
+            torch.cuda.synchronize()
+            assert h.last_error()[0] == 0, (rep, h.last_error(), h.stats().timeouts)
+            d = h.digest()
+            assert d.live_pages == 0 and d.partition_ok == 1, rep
