@@ -49,12 +49,14 @@ typedef struct ouro_queue_dev {
     uint32_t* dcnt;
     ouro_u64 seg_live;                 /* stats */
     ouro_u64 seg_hwm;
-    /* VirtualList lookup accelerator: links {seq:32|chunk:32} of the
-     * OURO_VL_RECENT most recently created segments at [seq % OURO_VL_RECENT].
+    /* VirtualList lookup accelerator: links {seq:32|chunk:32} of the most
+     * recently created segments (creation ring, sized per queue by the host).
      * The list itself stays the source of truth; an entry is used only when its
      * seq matches (a segment cannot retire while a caller still needs it). */
 #define OURO_VL_RECENT 256
-    ouro_u64 vl_recent[OURO_VL_RECENT];
+    ouro_u64* vl_recent;               /* device array of vl_rmask + 1 links at [seq & vl_rmask] */
+    ouro_u64 vl_rmask;                 /* ring size - 1: >= 2x the segments in-flight tickets can span */
+    ouro_u64 vl_recent_pad[OURO_VL_RECENT - 2];
     /* Dequeue-side accelerator: links of the segments at and ahead of the head at
      * [seq % OURO_VL_RECENT], kept ahead of consumption by the dequeuer that starts
      * each segment (ouro_device.cuh vl_extend_ring); walkers record every hop they

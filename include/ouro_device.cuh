@@ -530,9 +530,12 @@ __device__ __forceinline__ u64 mklink(u64 s, u32 c) { return ((u64)(u32)s << 32)
 __device__ __forceinline__ u32* vl_counter(const ouro_heap_view& v, u32 c) {
     return reinterpret_cast<u32*>(chunk_words(v, c) + 1);
 }
+// Upper half of header word 1: set once the predecessor links to this segment
+// (segment 0 and the prefilled segments start with it set).
+__device__ __forceinline__ u32* vl_inflag(const ouro_heap_view& v, u32 c) { return vl_counter(v, c) + 1; }
 
 // Find the chunk of segment s.  First the ring of recently created segments
-// (vl_recent, written by each creator right after it links its segment).
+// (vl_recent, written by each creator as soon as its chunk is ready).
 // from_tail (enqueuers, segment creators): the target is the newest segment or
 // one being created now, so a ring slot still holding an older segment means
 // "not created yet": wait on that slot (waiters of different segments poll
@@ -543,7 +546,7 @@ __device__ __forceinline__ bool vl_locate(const ouro_heap_view& v, ouro_queue_de
                                           bool from_tail = false) {
     Spin sp;
     for (;;) {
-        const u64 r = ld_rlx(&Q->vl_recent[s % OURO_VL_RECENT]);
+        const u64 r = ld_rlx(&Q->vl_recent[(s) & Q->vl_rmask]);
         const u64 d = from_tail ? NONE_LINK : ld_rlx(&Q->vl_deq[s % OURO_VL_RECENT]);  // issued together
         if (lchk(r) != NONE && lseq(r) == (u32)s) { *out = lchk(r); return true; }
         if (lchk(d) != NONE && lseq(d) == (u32)s) { *out = lchk(d); return true; }
@@ -699,32 +702,70 @@ __device__ __forceinline__ void vl_add(const ouro_heap_view& v, ouro_queue_dev* 
         vl_try_advance(v, Q, mask, lane, __ffs(dm) - 1);
     }
 }
+// A published segment's chunk from the creation ring, without waiting: NONE if
+// seq s is not in its slot; *newer: the slot already holds a later segment.
+__device__ __forceinline__ u32 vl_ring_peek(ouro_queue_dev* Q, u32 s, bool* newer) {
+    const u64 r = ld_rlx(&Q->vl_recent[(s) & Q->vl_rmask]);
+    *newer = lchk(r) != NONE && (int)(lseq(r) - s) > 0;
+    return (lchk(r) != NONE && lseq(r) == s) ? lchk(r) : NONE;
+}
+// Link segment s-1 (chunk p) to segment s (chunk c); true for the one caller that did.
+__device__ __forceinline__ bool vl_link(const ouro_heap_view& v, u32 p, u32 s, u32 c) {
+    if (atomicCAS(chunk_words(v, p), NONE_LINK, mklink(s, c)) != NONE_LINK) return false;
+    atomicExch(vl_inflag(v, c), 1u);
+    return true;
+}
+// Segment creation without a chain: the creator of s publishes its chunk in the
+// creation ring as soon as it is zeroed (the enqueuers of s need only that), then
+// links whichever neighbours are already published -- s-1 -> s and s -> s+1.
+// Each creator publishes, fences (seq-cst), then reads its neighbours' ring slots,
+// so of two adjacent creators at least one sees the other (store-buffering
+// litmus); the link word's CAS from NONE_LINK picks the one that links and counts
+// the link event on the predecessor's retire counter.  (Linking s into s-1 before
+// publishing s made the creations of a burst a serial chain: ~4 us per segment,
+// 497 us to free 2^20 16 B pages into 128 new VLPQ segments.)
+// A ring slot is reused only once its occupant is linked both ways (or retired),
+// so a neighbour missing from the ring because a later segment took its slot is
+// already linked to us; with tiny segments (thousands in flight) creators wait
+// here for the linking to catch up instead of losing a link.
 __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask, u32 lane,
                                           u32 who, u64 s) {
     const u32 c = seg_acquire_zero(v, Q, mask, lane, who);
     if (c == NONE) return false;
-    u32 p = NONE, ok = 1;
+    u32 back = NONE, fwd = 0, ok = 1;
     if (lane == who) {
         st_rlx(chunk_words(v, c), NONE_LINK);
-        __threadfence();
+        if (s == 0) st_rlx(reinterpret_cast<u64*>(vl_counter(v, c)), 1ull << 32);  // no predecessor: in-linked
+        __threadfence();  // the zeroed chunk and its header before the publication
         seg_count(Q, +1);
-        if (s == 0) {
-            st_rel(&Q->vl_head, mklink(0, c));
-            st_rel(&Q->vl_recent[0], mklink(0, c));
-            vl_tail_max(Q, mklink(0, c));
-        } else if (vl_locate(v, Q, s - 1, &p, true)) {
-            st_rel(chunk_words(v, p), mklink(s, c));
-            st_rel(&Q->vl_recent[s % OURO_VL_RECENT], mklink(s, c));  // wakes the waiters of s
-            vl_tail_max(Q, mklink(s, c));
-        } else {
-            ok = 0;
+        u64* slot = &Q->vl_recent[(s) & Q->vl_rmask];
+        Spin sp;
+        for (;;) {  // the slot's occupant must be fully linked (or retired) before we take it
+            const u64 r = ld_rlx(slot);
+            if (lchk(r) == NONE || (int)(lseq(r) - (u32)s) >= 0) break;
+            if ((int)(lseq(ld_rlx(&Q->vl_head)) - lseq(r)) > 0) break;  // retired
+            if (ld_rlx(chunk_words(v, lchk(r))) != NONE_LINK && ld_rlx32(vl_inflag(v, lchk(r))) != 0) break;
+            if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); ok = 0; break; }
         }
+        const u64 me = mklink(s, c);
+        if (s == 0) st_rlx(&Q->vl_head, me);
+        st_rlx(slot, me);  // publish: wakes the enqueuers of s
+        vl_tail_max(Q, me);
+        asm volatile("fence.sc.gpu;" ::: "memory");  // publication before the neighbour reads
+        bool newer;
+        if (s != 0) {
+            const u32 p = vl_ring_peek(Q, (u32)s - 1u, &newer);  // newer: s-1 fully linked already
+            if (p != NONE && vl_link(v, p, (u32)s, c)) back = p;
+        }
+        const u32 n = vl_ring_peek(Q, (u32)s + 1u, &newer);
+        if (n != NONE && vl_link(v, c, (u32)s + 1u, n)) fwd = 1;
     }
+    back = __shfl_sync(mask, back, who);
+    fwd = __shfl_sync(mask, fwd, who);
     ok = __shfl_sync(mask, ok, who);
-    p = __shfl_sync(mask, p, who);
-    if (!ok) return false;
-    if (s != 0) vl_add(v, Q, mask, lane, lane == who, p, 1u);  // link event
-    return true;
+    if (back != NONE) vl_add(v, Q, mask, lane, lane == who, back, 1u);  // link event of s-1
+    if (fwd) vl_add(v, Q, mask, lane, lane == who, c, 1u);              // link event of s
+    return ok != 0;
 }
 
 // ------------------------------------------------- flavour-generic queue ----

@@ -106,7 +106,7 @@ __global__ void k_vl_headers(uint8_t* heap, u32 chunk_shift, u32 seg0, u32 m) {
     if (i >= m) return;
     u64* w = reinterpret_cast<u64*>(heap + ((u64)(seg0 + i) << chunk_shift));
     w[0] = (i + 1 < m) ? (((u64)(i + 1) << 32) | (seg0 + i + 1)) : NONE_LINK;
-    w[1] = (i + 1 < m) ? 1ull : 0ull;
+    w[1] = (1ull << 32) | ((i + 1 < m) ? 1ull : 0ull);  // in-linked flag | retire counter (link event)
 }
 // Page-kind chunk headers: Reserved segment storage or Assigned(k) fully free.
 __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
@@ -520,7 +520,14 @@ ouro_status plan(ouro_heap* H) {
             q.dcnt = static_cast<u32*>(dalloc(H, (size_t)q.D * 4));
             return q.dir && q.dcnt;
         }
-        return true;
+        // VirtualList creation ring: at least twice the segments that the tickets
+        // of every resident thread (< 2^19 on B200) can span, so a ring entry
+        // outlives the enqueuers of its segment (256 at 64 KiB chunks; 16 Ki
+        // entries at 1 KiB chunks, where thousands of segments are in flight).
+        const u64 R = std::max<u64>(OURO_VL_RECENT, next_pow2(2 * ((1ull << 19) / S_vl + 2)));
+        q.vl_rmask = R - 1;
+        q.vl_recent = static_cast<u64*>(dalloc(H, R * 8));
+        return q.vl_recent != nullptr;
     };
     const u32 fl = H->cfg.queue_flavor;
     if (H->cfg.allocator_kind == OURO_KIND_PAGE) {
@@ -578,9 +585,9 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
     for (auto& q : H->hq) {
         q.count = 0; q.head = 0; q.tail = 0; q.seg_live = 0; q.seg_hwm = 0;
         q.vl_head = q.vl_tail = ((u64)0 << 32) | NONE;
-        for (auto& r : q.vl_recent) r = NONE_LINK;
         for (auto& r : q.vl_deq) r = NONE_LINK;
         q.vl_front = 0;
+        if (q.flavor == FL_VL && q.vl_recent) CK(cudaMemsetAsync(q.vl_recent, 0xFF, (q.vl_rmask + 1) * 8, st));
     }
     auto ring_fill = [&](ouro_queue_dev& q, u64 cap, int mode, u32 first, u32 ppc) -> ouro_status {
         const u64 R = q.ring_mask + 1;
@@ -634,8 +641,11 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
                 CK(cudaGetLastError());
                 q.vl_head = ((u64)0 << 32) | seg0;
                 q.vl_tail = ((u64)(m - 1) << 32) | (seg0 + m - 1);
-                for (u32 i = m > OURO_VL_RECENT ? m - OURO_VL_RECENT : 0; i < m; ++i)
-                    q.vl_recent[i % OURO_VL_RECENT] = ((u64)i << 32) | (seg0 + i);
+                const u64 R = q.vl_rmask + 1;
+                std::vector<u64> ring(R, NONE_LINK);
+                for (u64 i = m > R ? m - R : 0; i < m; ++i) ring[i & q.vl_rmask] = (i << 32) | (seg0 + i);
+                CK(cudaMemcpyAsync(q.vl_recent, ring.data(), R * 8, cudaMemcpyHostToDevice, st));
+                CK(cudaStreamSynchronize(st));
                 for (u32 i = 0; i < std::min<u32>(m, OURO_VL_RECENT); ++i)
                     q.vl_deq[i] = ((u64)i << 32) | (seg0 + i);
                 q.vl_front = std::min<u32>(m, OURO_VL_RECENT) - 1;

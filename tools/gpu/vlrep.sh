@@ -1,5 +1,5 @@
-# VL partition repro, current build: page kind VL / VA, chunk kind VL
-timeout 500 python tools/vl_partition_repro.py 0 2 10 > gpurun_out/vlrep_cur_2.log 2>&1
-timeout 300 python tools/vl_partition_repro.py 0 1 4 > gpurun_out/vlrep_cur_1.log 2>&1
-timeout 300 python tools/vl_partition_repro.py 1 2 4 > gpurun_out/vlrep_cur_c2.log 2>&1
-timeout 300 python bench.py --config vlpq8g --sizes 16,1024,8192 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/vlb.json 2>/dev/null
+# VirtualList stress: repeated 2^20-thread rounds + the tiny-segment tests, then the full GPU suite
+timeout 500 python tools/vl_partition_repro.py 0 2 8 > gpurun_out/vlrep_p.log 2>&1
+timeout 300 python tools/vl_partition_repro.py 1 2 5 > gpurun_out/vlrep_c.log 2>&1
+for i in 1 2 3; do timeout 300 python -m pytest tests -m gpu -x -q -k "virtual_segment_stress" 2>&1 | tail -1 >> gpurun_out/vlrep_vss.log; done
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5 > gpurun_out/gpu_tests.log
