@@ -138,10 +138,10 @@ struct Spin {
 #ifndef OURO_FENCE_SCOPE_GPU
 #define OURO_FENCE_SCOPE_GPU 0
 #endif
-__device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
-    if (v.backoff == OURO_BACKOFF_SLEEP) {
-        u64 ns = attempt >= 40 ? v.sleep_cap_ns : ((u64)v.sleep_base_ns << attempt);
-        if (ns > v.sleep_cap_ns) ns = v.sleep_cap_ns;
+__device__ __forceinline__ void backoff_policy(u32 policy, u32 base_ns, u32 cap_ns, u32 attempt) {
+    if (policy == OURO_BACKOFF_SLEEP) {
+        u64 ns = attempt >= 40 ? cap_ns : ((u64)base_ns << attempt);
+        if (ns > cap_ns) ns = cap_ns;
         __nanosleep((u32)ns);
     } else {
 #if OURO_FENCE_SCOPE_GPU
@@ -150,6 +150,9 @@ __device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
         asm volatile("fence.sc.cta;" ::: "memory");
 #endif
     }
+}
+__device__ __forceinline__ void backoff(const ouro_heap_view& v, u32 attempt) {
+    backoff_policy(v.backoff, v.sleep_base_ns, v.sleep_cap_ns, attempt);
 }
 
 // size_class_of; size 0 rejected like TooLarge (gap G5).
@@ -266,7 +269,7 @@ __device__ __forceinline__ u32 poll_seq_now(u64 tag) {
 // one in flight, or issues one.
 __device__ __forceinline__ u32 obs_seq(u32 o) { return o >> 1; }
 __device__ __forceinline__ bool obs_empty(u32 o) { return (o & 1u) != 0; }
-static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
+__device__ __forceinline__ u32 poll_after_inl(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
     u64* slot = poll_slot(tag);
     for (int spins = 0; spins < 4096; ++spins) {
         const u32 now = gtime32();
@@ -282,10 +285,17 @@ static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 
         const u32 empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
 
         atomicCAS(slot, fl, mk_entry(now, ns, tag, empty));  // unless a stale-entry reset replaced it
-        publish_hint(smh, tag, mk_entry(now, 0, tag, empty));
+#ifndef OURO_SMH_POLL_PUBLISH
+#define OURO_SMH_POLL_PUBLISH 1
+#endif
+        publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tag, mk_entry(now, 0, tag, empty));
         return (ns << 1) | empty;
     }
     return (((after + 1u) & kSeqMask) << 1) | ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u);
+}
+// Out-of-line form for the one-off callers (first-try hints, pre-checks).
+static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
+    return poll_after_inl(Q, floor, tag, after, smh);
 }
 
 // Pre-check before a reservation RMW (hint: the RMW decides).  One LDS, one
@@ -301,28 +311,33 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64
 // block-combined observation of the class queue (and, for the chunk kind, of
 // the pool) newer than the previous round's; stops when one sees work
 // (returns false) or when the budget is spent (returns true: OutOfMemory).
-// *attempt counts rounds as the oracle does.
-__device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
-                                            i64 pfloor, u32* attempt) {
-    u32 a = *attempt;
-    const u32 maxr = v.max_retries;
-    u64* smh = sm_hint_row(v);
+// *attempt counts rounds as the oracle does.  The round loop is ONE out-of-line
+// call with the polls inlined and scalar arguments: a call per round made the
+// caller spill its live state to local memory around every round.
+static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
+                                                    u32 maxr, u32 policy, u32 base_ns, u32 cap_ns, u64* smh) {
     const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
     u32 lq = poll_seq_now(tq), lp = P ? poll_seq_now(tp) : 0;  // read after the failed try returned
     for (;;) {
-        if (++a >= maxr) { *attempt = a; return true; }
-        backoff(v, a);
-        const u32 oq = poll_after(Q, 0, tq, lq, smh);
+        if (++a >= maxr) return (a << 1) | 1u;
+        backoff_policy(policy, base_ns, cap_ns, a);
+        const u32 oq = poll_after_inl(Q, 0, tq, lq, smh);
         lq = obs_seq(oq);
         if (!obs_empty(oq)) break;
         if (P) {
-            const u32 op = poll_after(P, pfloor, tp, lp, smh);
+            const u32 op = poll_after_inl(P, pfloor, tp, lp, smh);
             lp = obs_seq(op);
             if (!obs_empty(op)) break;
         }
     }
-    *attempt = a;
-    return false;
+    return a << 1;
+}
+__device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
+                                            i64 pfloor, u32* attempt) {
+    const u32 r = fail_rounds_loop(Q, P, pfloor, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
+                                   v.sleep_cap_ns, sm_hint_row(v));
+    *attempt = r >> 1;
+    return (r & 1u) != 0;
 }
 
 // Did this block recently see the queue empty?  (hint only: it just turns the
