@@ -35,9 +35,10 @@ __global__ void lists(ouro_heap_view h, int len, unsigned long long* bad) {
 }
 
 int main(int argc, char** argv) {
-    // optional: argv[1] = variant name to run alone
+    // optional: argv[1] = variant name to run alone ("all" = every variant), argv[2] = blocks
+    const int blocks = argc > 2 ? std::atoi(argv[2]) : 512;
     for (auto v : ouro::kAllVariants) {
-        if (argc > 1 && ouro::variant_name(v) != argv[1]) continue;
+        if (argc > 1 && std::string(argv[1]) != "all" && ouro::variant_name(v) != argv[1]) continue;
         ouro::HeapConfig cfg;                     // reference defaults: 64 MiB, 64 KiB chunks
         cfg.heap_bytes = 256ull << 20;
         cfg.allocator_kind = v.kind;
@@ -47,7 +48,7 @@ int main(int argc, char** argv) {
         unsigned long long* bad;
         cudaMalloc(&bad, 8);
         cudaMemset(bad, 0, 8);
-        lists<<<512, 256>>>(view, 8, bad);
+        lists<<<blocks, 256>>>(view, 8, bad);
         if (second_tu_check(view) != 0) { std::printf("second TU failed\n"); return 1; }
         unsigned long long hb = 0;
         cudaMemcpy(&hb, bad, 8, cudaMemcpyDeviceToHost);
