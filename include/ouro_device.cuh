@@ -1112,7 +1112,10 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             oldfree = __shfl_sync(mask, oldfree, leader);
             if (!take) continue;
             const u32 page = warp_claim(v, c, k, take, mask, lane, (intodo && rank < take) ? rank : NONE);
-            q_enqueue<FL>(v, k, mask, lane, (oldfree - take > 0) ? (1u << leader) : 0u, e);  // in-transit rule
+            // in-transit rule: the holder puts its entry back.  It cannot overflow the
+            // queue -- our own dequeue freed a ring position and its count -- so the count
+            // update is a fire-and-forget add instead of a capacity-checked RMW round trip.
+            q_enqueue<FL>(v, k, mask, lane, (oldfree - take > 0) ? (1u << leader) : 0u, e, true);
             if (intodo && rank < take) {
                 if (page != NONE) {
                     *res = v.base + ((u64)c << v.chunk_shift) + ((u64)page << (v.min_shift + k));
