@@ -259,6 +259,25 @@ def _traffic():
         return None
 
 
+def storm_roofline(per_size, n, max_retries, hot_lat_s, block, resident_per_sm=6, sms=148):
+    """Latency roofline of the OOM-heavy alloc launches (> half the requests OOM): a warp
+    that fails declares OutOfMemory only after max_retries - 1 further rounds, each needing
+    an observation of the queue made after the previous one, i.e. one
+    dependent hot-word load per round at best; blocks run in n / (block x resident) waves.
+    floor = waves x (max_retries - 1) x measured hot-word load latency (ouro_atomic_peak
+    mode 4: 888 concurrent pollers of one word, the storm's contention)."""
+    waves = n / (block * resident_per_sm * sms)
+    floor_us = waves * (max_retries - 1) * hot_lat_s * 1e6
+    out = {}
+    for s, p in per_size.items():
+        if p["oom"] * 2 > n:
+            out[s] = {"alloc_us": p["alloc_us"], "floor_us": round(floor_us, 1),
+                      "frac": round(floor_us / p["alloc_us"], 3)}
+    return {"bound": "latency", "resource": "one dependent L2 load of the class-queue count per retry round",
+            "hot_load_ns": round(hot_lat_s * 1e9, 1), "waves": round(waves, 2),
+            "rounds": max_retries - 1, "per_size": out}
+
+
 def job_totals(tot_ms, tot_ok, world, device):
     """Whole-job totals for weak scaling: time = MAX over ranks of the device
     time, work = SUM over ranks of successful pairs (independent heaps, no
@@ -311,6 +330,7 @@ def main():
     # roofline denominators measured on this device
     p_same = ob.atomic_peak(local, 2)      # same-address RMW, one per warp
     p_dist = ob.atomic_peak(local, 0)      # distinct-address 32-bit RMW, one per sector
+    hot_lat_s = 1.0 / ob.atomic_peak(local, 4)  # hot-word dependent load latency, 888 pollers
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
     per = {s: {"alloc_ms": [], "free_ms": [], "write_ms": [], "verify_ms": [], "ok": [], "verify_bad": 0}
@@ -483,6 +503,7 @@ def main():
                                      "peak_gops": p_dist / 1e9,
                                      "frac": elem_ops / ((a_ms + f_ms) / 1e3) / p_dist},
                      "dominant_kernel_share": dom_ms / (a_ms + f_ms),
+                     "oom_storm": storm_roofline(per_size, n, hc.max_retries, hot_lat_s, args.block),
                      "note": "sweep-level: the OOM-heavy sizes spend their alloc time in the SPEC's "
                              "max_retries rounds, not on the RMW chain; per_size[*].alloc_roofline_frac "
                              "gives the fraction where all threads are served"},

@@ -296,7 +296,10 @@ ouro_status ouro_trial_means(const double* ms, uint32_t n, double* mean_all, dou
 /* ---------------- micro-benchmarks for the roofline denominators ---------------- */
 /* mode 0: distinct-address 32-bit atomicAdd (one per 32 B sector, coalesced);
  * mode 1: distinct-address 64-bit atomicCAS; mode 2: same-address atomicAdd, one
- * per warp (aggregated); mode 3: same-address atomicAdd from every lane.
+ * per warp (aggregated); mode 3: same-address atomicAdd from every lane;
+ * mode 4: 888 blocks (6 per SM) each issue 256 dependent .relaxed.gpu loads of
+ * ONE word -- the retry-round poll of an OOM storm -- and the result is the
+ * loads per second of one poller (1 / hot-word latency under that contention).
  * Returns element-ops per second measured with CUDA events. */
 ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s);
 

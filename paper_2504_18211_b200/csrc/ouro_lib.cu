@@ -443,6 +443,16 @@ __global__ void k_atom_same_warp(u64* a, u32 iters) {
     }
     if (acc == ~0ull) a[1] = acc;
 }
+// One leader lane per block loads ONE word back to back, each load's address
+// depending on the previous result: the retry-round poll pattern of an OOM storm.
+__global__ void k_hot_poll(const u64* a, u32 iters, u64* cyc) {
+    if (threadIdx.x) return;
+    u64 acc = 0;
+    const u64 c0 = clock64();
+    for (u32 r = 0; r < iters; ++r) acc += ld_rlx(a + (acc >> 63));
+    if (acc == 12345) cyc[1] = acc;  // consume before the clock read
+    atomicAdd(cyc, clock64() - c0);
+}
 __global__ void k_atom_same_lane(u64* a, u32 iters) {
     u64 acc = 0;
     for (u32 r = 0; r < iters; ++r) {
@@ -1258,6 +1268,7 @@ ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
         case 0: k_atom_distinct32<<<blocks, threads>>>((u32*)buf, words * 2, iters); break;
         case 1: k_atom_distinct_cas64<<<blocks, threads>>>((u64*)buf, words, iters); break;
         case 2: k_atom_same_warp<<<blocks, threads>>>((u64*)buf, iters); break;
+        case 4: k_hot_poll<<<148 * 6, 32>>>((const u64*)buf, 2048, (u64*)buf + 64); break;
         default: k_atom_same_lane<<<blocks, threads>>>((u64*)buf, iters / 16); break;
         }
     };
@@ -1277,6 +1288,7 @@ ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     double ops = (double)blocks * threads * iters;
     if (mode == 2) ops /= 32.0;
     if (mode == 3) ops = (double)blocks * threads * (iters / 16);
+    if (mode == 4) ops = 2048.0;  // loads of ONE poller (all 888 run concurrently): 1 / hot-word latency
     *ops_per_s = ops / (best * 1e-3);
     cudaEventDestroy(a);
     cudaEventDestroy(b);
