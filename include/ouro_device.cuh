@@ -397,7 +397,11 @@ __device__ __forceinline__ void reserve_enq_nofull(ouro_queue_dev* Q, u32 n) {
     atomicAdd((u64*)&Q->count, (u64)n);
 }
 
-__device__ __forceinline__ u32 vtag(u64 t) { return ((u32)t & 0x7FFFFFFFu) | 0x80000000u; }
+// Tag of a filled virtual-queue slot: the segment's sequence number (each slot
+// of a segment is written once per segment life), so a recycled segment chunk's
+// old tags never match: a collision needs the same chunk to serve segments 2^31
+// apart.  (A ticket-based tag would collide after 2^31 tickets.)  Empty = 0.
+__device__ __forceinline__ u32 vtag_seg(u64 seg) { return ((u32)seg & 0x7FFFFFFFu) | 0x80000000u; }
 
 // ---------------------------------------------------------- Array slots ----
 // slot t&mask in round r = t>>shift: tag 2r empty, 2r+1 full.
@@ -495,11 +499,18 @@ __device__ __forceinline__ u32 seg_acquire_zero(const ouro_heap_view& v, ouro_qu
     }
     c = __shfl_sync(mask, c, who);
     if (c == NONE) return NONE;
-    const u32 L = __popc(mask), li = __popc(mask & lanemask_lt());
-    u64* w = chunk_words(v, c);
-    const u64 nw = v.chunk_bytes / 8;
-    for (u64 i = 2ull * li; i < nw; i += 2ull * L) st_zero_v2(w + i);
-    __threadfence();
+    // Chunks from the shared chunk pool (chunk kind) held payload, which could
+    // look like a filled slot: zero them.  A page kind's private segment pool
+    // only ever holds segment chunks (zeroed at heap creation) whose stale slot
+    // tags name older segments, so only the header words need resetting (the
+    // creators do that).
+    if (v.kind == KIND_CHUNK) {
+        const u32 L = __popc(mask), li = __popc(mask & lanemask_lt());
+        u64* w = chunk_words(v, c);
+        const u64 nw = v.chunk_bytes / 8;
+        for (u64 i = 2ull * li; i < nw; i += 2ull * L) st_zero_v2(w + i);
+        __threadfence();
+    }
     __syncwarp(mask);
     return c;
 }
@@ -750,7 +761,9 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
     u32 back = NONE, fwd = 0, ok = 1;
     if (lane == who) {
         st_rlx(chunk_words(v, c), NONE_LINK);
-        if (s == 0) st_rlx(reinterpret_cast<u64*>(vl_counter(v, c)), 1ull << 32);  // no predecessor: in-linked
+        // retire counter 0, in-link flag set only for segment 0 (no predecessor); the
+        // chunk may not have been zeroed
+        st_rlx(reinterpret_cast<u64*>(vl_counter(v, c)), s == 0 ? (1ull << 32) : 0ull);
         __threadfence();  // the zeroed chunk and its header before the publication
         seg_count(Q, +1);
         u64* slot = &Q->vl_recent[(s) & Q->vl_rmask];
@@ -811,7 +824,7 @@ template <int FL>
 __device__ __forceinline__ bool q_put(const ouro_heap_view& v, ouro_queue_dev* Q, u64 t, u32 val, u32 c) {
     if (FL == FL_ARRAY) return arr_put(v, Q, t, val);
     if (c == NONE) return false;
-    st_rlx(slot_in<FL>(v, c, t), ((u64)vtag(t) << 32) | val);
+    st_rlx(slot_in<FL>(v, c, t), ((u64)vtag_seg(t / seg_slots<FL>(v)) << 32) | val);
     return true;
 }
 template <int FL>
@@ -821,7 +834,8 @@ __device__ __forceinline__ bool q_take(const ouro_heap_view& v, ouro_queue_dev* 
     u64* s = slot_in<FL>(v, c, t);
     Spin sp;
     u64 x;
-    while ((u32)((x = ld_rlx(s)) >> 32) != vtag(t))
+    const u32 want = vtag_seg(t / seg_slots<FL>(v));
+    while ((u32)((x = ld_rlx(s)) >> 32) != want)
         if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); return false; }
     *val = (u32)x;
     return true;

@@ -98,7 +98,7 @@ __global__ void k_fill_segments(uint8_t* heap, u32 chunk_shift, u32 seg0, u64 S,
         const u32 c = seg0 + (u32)(t / S);
         u64* w = reinterpret_cast<u64*>(heap + ((u64)c << chunk_shift));
         const u32 val = ((first_chunk + (u32)(t / ppc)) << page_bits) | (u32)(t % ppc);
-        w[hdr + t % S] = ((u64)vtag(t) << 32) | val;
+        w[hdr + t % S] = ((u64)vtag_seg(t / S) << 32) | val;
     }
 }
 __global__ void k_vl_headers(uint8_t* heap, u32 chunk_shift, u32 seg0, u32 m) {
@@ -635,7 +635,9 @@ ouro_status fill(ouro_heap* H, cudaStream_t st) {
             const u64 Sx = fl == FL_VA ? S_va : S_vl;
             const u32 m = (u32)((cap + Sx - 1) / Sx);
             const u32 seg0 = H->pq_start[k];
-            if (m) CK(cudaMemsetAsync(H->d_heap + ((u64)seg0 << g.chunk_shift), 0, (size_t)m << g.chunk_shift, st));
+            // every segment chunk of the class, prefilled or in the private pool, starts
+            // zeroed: recycled ones are never zeroed again (seg_acquire_zero)
+            if (s) CK(cudaMemsetAsync(H->d_heap + ((u64)seg0 << g.chunk_shift), 0, (size_t)s << g.chunk_shift, st));
             if (cap) {
                 k_fill_segments<<<std::min<u64>((cap + kBlock - 1) / kBlock, 148 * 64), kBlock, 0, st>>>(
                     H->d_heap, g.chunk_shift, seg0, Sx, fl == FL_VA ? 0 : 2, cap, first, ppc, g.page_bits);
