@@ -251,9 +251,9 @@ def rmw_per_pair(kind, flavor, size, chunk=64 << 10):
 
 def _traffic():
     """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r1b_traffic.json): the 16 B launch, where all threads are served."""
+    capture (profiles/r1c_traffic.json): the 16 B launch, where all threads are served."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1b_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r1c_traffic.json")) as f:
             return json.load(f)["per_launch_dram_bytes"]["16"]
     except Exception:
         return None
