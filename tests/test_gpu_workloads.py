@@ -337,3 +337,28 @@ def test_virtual_list_retirement_under_load(cuda, kind):
             assert h.last_error()[0] == 0, (rep, h.last_error(), h.stats().timeouts)
             d = h.digest()
             assert d.live_pages == 0 and d.partition_ok == 1, rep
+
+
+@pytest.mark.parametrize("flavor", [1, 2])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_virtual_churn_small_segments(cuda, kind, flavor):
+    """Mixed alloc/free rounds in one kernel on 4 KiB chunks (510 / 512-slot
+    segments): segment creation, linking and retirement interleave with
+    enqueues and dequeues of the same queue inside each launch.  Stamps every
+    round, audit, then free-all to an exact partition with no device error."""
+    torch = cuda
+    n = 1 << 16
+    with ob.Heap(_hc(kind, flavor, 64 << 20, chunk=4096, maxp=4096)) as h:
+        slots = torch.zeros(n, dtype=torch.int64, device="cuda")
+        res = torch.zeros(5, dtype=torch.int64, device="cuda")
+        h.launch_churn(n, 0, 30, 7, slots, res)
+        torch.cuda.synchronize()
+        ok, failed, frees, reused, bad = [int(x) for x in res]
+        assert bad == 0 and ok > 0 and frees > 0
+        a = h.audit(n, slots)
+        assert a.overlaps == 0 and a.out_of_heap == 0 and a.misaligned == 0 and a.not_marked == 0
+        h.launch_free(n, slots)
+        torch.cuda.synchronize()
+        assert h.last_error()[0] == 0, (h.last_error(), h.stats().timeouts)
+        d = h.digest()
+        assert d.live_pages == 0 and d.partition_ok == 1
