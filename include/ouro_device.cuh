@@ -540,10 +540,10 @@ __device__ __forceinline__ bool va_create(const ouro_heap_view& v, ouro_queue_de
     const u32 c = seg_acquire_zero(v, Q, mask, lane, who);
     if (c == NONE) return false;
     if (lane == who) {
-        atomicExch(Q->dcnt + (s % Q->D), 0u);
-        __threadfence();
-        st_rel(e, ((u64)(u32)s << 32) | c);
-        seg_count(Q, +1);
+        *reinterpret_cast<volatile u32*>(Q->dcnt + (s % Q->D)) = 0u;
+        __threadfence();  // the dequeue count (and a zeroed chunk) before the publication
+        st_rlx(e, ((u64)(u32)s << 32) | c);
+        seg_count(Q, +1);  // statistics, after the publication that the enqueuers wait for
     }
     __syncwarp(mask);
     return true;
@@ -765,7 +765,6 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
         // chunk may not have been zeroed
         st_rlx(reinterpret_cast<u64*>(vl_counter(v, c)), s == 0 ? (1ull << 32) : 0ull);
         __threadfence();  // the zeroed chunk and its header before the publication
-        seg_count(Q, +1);
         u64* slot = &Q->vl_recent[(s) & Q->vl_rmask];
         Spin sp;
         for (;;) {  // the slot's occupant must be fully linked (or retired) before we take it
@@ -778,6 +777,7 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
         const u64 me = mklink(s, c);
         if (s == 0) st_rlx(&Q->vl_head, me);
         st_rlx(slot, me);  // publish: wakes the enqueuers of s
+        seg_count(Q, +1);
         vl_tail_max(Q, me);
         asm volatile("fence.sc.gpu;" ::: "memory");  // publication before the neighbour reads
         bool newer;
