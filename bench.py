@@ -278,6 +278,22 @@ def storm_roofline(per_size, n, max_retries, hot_lat_s, block, resident_per_sm=6
             "rounds": max_retries - 1, "per_size": out}
 
 
+def sweep_floor(per_size, n, max_retries, hot_lat_s, block, p_same):
+    """The alloc kernel's floor over the whole sweep: per size, the same-address chain
+    floor (ceil(ok/32) RMWs per chain address at the measured same-address peak) or,
+    for OOM-heavy sizes, the retry-round latency floor (storm_roofline); summed and
+    compared with the summed measured alloc time."""
+    storm = storm_roofline(per_size, n, max_retries, hot_lat_s, block)["per_size"]
+    floor = actual = 0.0
+    for s, p in per_size.items():
+        chain_us = (p["ok"] + 31) // 32 / p_same * 1e6
+        floor += max(chain_us, storm[s]["floor_us"]) if s in storm else chain_us
+        actual += p["alloc_us"]
+    return {"floor_us": round(floor, 1), "alloc_us": round(actual, 1),
+            "frac": round(floor / actual, 3) if actual else None,
+            "model": "sum over sizes of max(chain floor, OOM-round latency floor) / sum of alloc times"}
+
+
 def job_totals(tot_ms, tot_ok, world, device):
     """Whole-job totals for weak scaling: time = MAX over ranks of the device
     time, work = SUM over ranks of successful pairs (independent heaps, no
@@ -504,6 +520,7 @@ def main():
                                      "frac": elem_ops / ((a_ms + f_ms) / 1e3) / p_dist},
                      "dominant_kernel_share": dom_ms / (a_ms + f_ms),
                      "oom_storm": storm_roofline(per_size, n, hc.max_retries, hot_lat_s, args.block),
+                     "sweep_floor": sweep_floor(per_size, n, hc.max_retries, hot_lat_s, args.block, p_same),
                      "note": "sweep-level: the OOM-heavy sizes spend their alloc time in the SPEC's "
                              "max_retries rounds, not on the RMW chain; per_size[*].alloc_roofline_frac "
                              "gives the fraction where all threads are served"},

@@ -36,3 +36,14 @@ def test_rmw_per_pair_matches_survey_table():
 
 def test_page_bytes_rounds_to_class():
     assert [bench.page_bytes(s) for s in (4, 16, 17, 1000, 1024, 8192)] == [16, 16, 32, 1024, 1024, 8192]
+
+
+def test_sweep_floor_mixes_chain_and_storm_floors():
+    n = 1 << 20
+    per = {"16": {"ok": n, "oom": 0, "alloc_us": 36.0},
+           "8192": {"ok": 13104, "oom": n - 13104, "alloc_us": 236.0}}
+    r = bench.sweep_floor(per, n, 64, 220e-9, 256, p_same=1.45e9)
+    chain16 = (n // 32) / 1.45e9 * 1e6
+    storm = bench.storm_roofline(per, n, 64, 220e-9, 256)["per_size"]["8192"]["floor_us"]
+    assert abs(r["floor_us"] - round(chain16 + storm, 1)) < 0.2
+    assert r["alloc_us"] == 272.0 and 0 < r["frac"] < 1
