@@ -194,8 +194,8 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 // "Issued after" is a per-(block, queue) poll sequence number, not a clock:
 // polls of one entry are issued one at a time and each only after the
 // previous one completed, so a higher sequence number was issued later.  (An
-// ordering by %globaltimer ticks made every round wait for the next tick:
-// ~1 us per round, 372 us per OOM-storm launch.)
+// ordering by %globaltimer ticks made every round wait for the next 256 ns
+// tick.)
 // Poll entry: [63:32] issue time (globaltimer / 256 ns), [31:8] sequence,
 // [7:3] queue tag, [1] in flight, [0] empty.  Hint entry (first-try hints and
 // pre-checks only, never a round's observation): [63:32] time, [7:3] tag,
