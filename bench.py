@@ -374,7 +374,7 @@ def main():
             ev[3].record()
             ev[3].synchronize()
             if record:
-                launches += 2
+                launches += 5  # ours per size: alloc, count, write, verify, free
                 p = per[s]
                 p["alloc_ms"].append(ev[0].elapsed_time(ev[1]))
                 p["free_ms"].append(ev[2].elapsed_time(ev[3]))

@@ -161,54 +161,69 @@ __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p
     return 1ull << (v.min_shift + st - 1);
 }
 
-// Pattern writer / verifier.  Regions of >= 512 B are
-// processed by the whole warp (16 B per lane per store, coalesced); smaller
-// ones by their own thread.
+// Pattern writer / verifier.  Warp w covers the slot group
+// {g + k*G : lane k < 32}, G = ceil(n / 32): regions under 512 B are done by
+// their own lane (16 B vector accesses), regions of >= 512 B by the whole warp
+// (16 B per lane, 512 B coalesced per access).  Striding a group over the slot
+// range spreads the live slots of an OOM-heavy launch -- the first ones (8 KiB:
+// 13 104 of 2^20) -- over thousands of warps; with a warp per 32 consecutive
+// slots, ~400 warps did all of that work one page after another (verify ran at
+// ~0.4 TB/s; now 8 KiB write 4.4 TB/s, verify 2.3 TB/s).  The price: a lane's
+// small regions are no longer next to its neighbours', so writes of 16-64 B
+// regions coalesce less (16 B: 1.5 -> 1.0 TB/s over a 16 MiB, launch-bound pass).
 template <bool VERIFY>
 __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, void* const* ptrs, u64 seed, u32 it,
                                                     u64* result) {
-    const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
     const u32 lane = threadIdx.x & 31;
-    void* p = i < n ? ptrs[i] : nullptr;
-    const u64 len = p ? region_len(v, p) : 0;
+    const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
+    const u64 G = (n + 31) / 32;
     u64 bad = 0;
-    const u32 big = __ballot_sync(0xFFFFFFFFu, len >= 512);
-    if (len && len < 512) {
-        const u64 b = pattern_base(seed, i, it);
-        u64* w = reinterpret_cast<u64*>(p);
-        for (u64 j = 0; j < len / 8; j += 2) {
-            if (VERIFY) {
-                const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
-                bad += (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
-            } else {
-                reinterpret_cast<ulonglong2*>(w)[j / 2] = make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+    for (u64 g = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; g < G; g += nwarps) {
+        const u64 i = g + lane * G;
+        void* p = i < n ? ptrs[i] : nullptr;
+        const u64 len = p ? region_len(v, p) : 0;
+        if (len && len < 512) {
+            const u64 b = pattern_base(seed, i, it);
+            u64* w = reinterpret_cast<u64*>(p);
+            u64 nb = 0;
+            for (u64 j = 0; j < len / 8; j += 2) {
+                if (VERIFY) {
+                    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
+                    nb += (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
+                } else {
+                    reinterpret_cast<ulonglong2*>(w)[j / 2] =
+                        make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+                }
             }
+            if (VERIFY && nb) { bad += nb; atomicMin(&result[1], i); }
         }
-    }
-    u32 it_mask = big;
-    while (it_mask) {
-        const u32 src = __ffs(it_mask) - 1;
-        u64* w = reinterpret_cast<u64*>(__shfl_sync(0xFFFFFFFFu, (u64)p, src));
-        const u64 L = __shfl_sync(0xFFFFFFFFu, len, src);
-        const u64 slot = i - lane + src;
-        const u64 b = pattern_base(seed, slot, it);
-        for (u64 j = 2 * lane; j < L / 8; j += 64) {
-            if (VERIFY) {
-                const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
-                const u64 nb = (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
-                if (nb) { bad += nb; atomicMin(&result[1], slot); }
-            } else {
-                reinterpret_cast<ulonglong2*>(w)[j / 2] = make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+        u32 todo = __ballot_sync(0xFFFFFFFFu, len >= 512);
+        while (todo) {
+            const u32 src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            u64* w = reinterpret_cast<u64*>(__shfl_sync(0xFFFFFFFFu, (u64)p, src));
+            const u64 L = __shfl_sync(0xFFFFFFFFu, len, src);
+            const u64 slot = g + src * G;
+            const u64 b = pattern_base(seed, slot, it);
+            u64 nb = 0;
+            for (u64 j = 2 * lane; j < L / 8; j += 64) {
+                if (VERIFY) {
+                    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
+                    nb += (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
+                } else {
+                    reinterpret_cast<ulonglong2*>(w)[j / 2] =
+                        make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+                }
             }
+            if (VERIFY && nb) { bad += nb; atomicMin(&result[1], slot); }
         }
-        it_mask &= it_mask - 1;
     }
     if (VERIFY) {
-        if (bad && len && len < 512) atomicMin(&result[1], i);
         for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
         if (lane == 0 && bad) atomicAdd(&result[0], bad);
     }
 }
+unsigned pattern_grid(u64 n) { return (unsigned)std::max<u64>(1, ((n + 31) / 32 + 7) / 8); }  // one group per warp
 
 __global__ void k_count(u64 n, void* const* ptrs, u64* count) {
     const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;
@@ -1089,7 +1104,7 @@ ouro_status ouro_launch_free(ouro_heap* H, uint64_t n, void* const* d_ptrs, void
 ouro_status ouro_launch_write(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t seed, uint32_t it, void* stream) {
     if (!H || !d_ptrs) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
-    k_pattern<false><<<grid_for(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, nullptr);
+    k_pattern<false><<<pattern_grid(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, nullptr);
     CK(cudaGetLastError());
     return OURO_OK;
 }
@@ -1098,7 +1113,8 @@ ouro_status ouro_launch_verify(ouro_heap* H, uint64_t n, void* const* d_ptrs, ui
                                uint64_t* d_result, void* stream) {
     if (!H || !d_ptrs || !d_result) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
-    k_pattern<true><<<grid_for(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, reinterpret_cast<u64*>(d_result));
+    k_pattern<true><<<pattern_grid(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it,
+                                                              reinterpret_cast<u64*>(d_result));
     CK(cudaGetLastError());
     return OURO_OK;
 }
