@@ -161,6 +161,9 @@ __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p
     return 1ull << (v.min_shift + st - 1);
 }
 
+#ifndef OURO_PAT_RUN
+#define OURO_PAT_RUN 2
+#endif
 // Pattern writer / verifier.  Warp w covers the slot group
 // {g + k*G : lane k < 32}, G = ceil(n / 32): regions under 512 B are done by
 // their own lane (16 B vector accesses), regions of >= 512 B by the whole warp
@@ -168,18 +171,27 @@ __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p
 // range spreads the live slots of an OOM-heavy launch -- the first ones (8 KiB:
 // 13 104 of 2^20) -- over thousands of warps; with a warp per 32 consecutive
 // slots, ~400 warps did all of that work one page after another (verify ran at
-// ~0.4 TB/s; now 8 KiB write 4.4 TB/s, verify 2.3 TB/s).  The price: a lane's
-// small regions are no longer next to its neighbours', so writes of 16-64 B
-// regions coalesce less (16 B: 1.5 -> 1.0 TB/s over a 16 MiB, launch-bound pass).
+// ~0.4 TB/s; now 8 KiB write 4.0 TB/s, verify 2.3 TB/s).  Lanes work in runs of
+// OURO_PAT_RUN consecutive slots so small regions still coalesce in pairs (runs
+// of 1 / 2 / 4 / 8, 16 B write: 0.9 / 1.4 / 1.4 / 1.4 TB/s; 8 KiB: 4.0 / 4.0 /
+// 3.3 / 2.4 TB/s).
+// lanes in runs of kPatRun consecutive slots (so small regions coalesce per run),
+// the 32 / kPatRun runs of a warp strided Q slots apart over the slot range
+constexpr u32 kPatRun = OURO_PAT_RUN;
+__device__ __forceinline__ u64 slot_of(u64 g, u32 lane, u64 Q) {
+    return g * kPatRun + (lane % kPatRun) + (u64)(lane / kPatRun) * Q;
+}
 template <bool VERIFY>
 __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, void* const* ptrs, u64 seed, u32 it,
                                                     u64* result) {
     const u32 lane = threadIdx.x & 31;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
-    const u64 G = (n + 31) / 32;
+    const u64 runs = 32 / kPatRun;                                        // lane runs per warp
+    const u64 Q = ((n + runs - 1) / runs + kPatRun - 1) / kPatRun * kPatRun;  // slots per run column
+    const u64 G = Q / kPatRun;
     u64 bad = 0;
     for (u64 g = (blockIdx.x * (u64)blockDim.x + threadIdx.x) >> 5; g < G; g += nwarps) {
-        const u64 i = g + lane * G;
+        const u64 i = slot_of(g, lane, Q);
         void* p = i < n ? ptrs[i] : nullptr;
         const u64 len = p ? region_len(v, p) : 0;
         if (len && len < 512) {
@@ -203,7 +215,7 @@ __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, voi
             todo &= todo - 1;
             u64* w = reinterpret_cast<u64*>(__shfl_sync(0xFFFFFFFFu, (u64)p, src));
             const u64 L = __shfl_sync(0xFFFFFFFFu, len, src);
-            const u64 slot = g + src * G;
+            const u64 slot = slot_of(g, src, Q);
             const u64 b = pattern_base(seed, slot, it);
             u64 nb = 0;
             for (u64 j = 2 * lane; j < L / 8; j += 64) {
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, voi
         if (lane == 0 && bad) atomicAdd(&result[0], bad);
     }
 }
-unsigned pattern_grid(u64 n) { return (unsigned)std::max<u64>(1, ((n + 31) / 32 + 7) / 8); }  // one group per warp
+unsigned pattern_grid(u64 n) { return (unsigned)std::max<u64>(1, ((n + 31) / 32 + 7) / 8); }  // ~one group per warp
 
 __global__ void k_count(u64 n, void* const* ptrs, u64* count) {
     const u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x;

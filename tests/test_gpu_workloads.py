@@ -362,3 +362,31 @@ def test_virtual_churn_small_segments(cuda, kind, flavor):
         assert h.last_error()[0] == 0, (h.last_error(), h.stats().timeouts)
         d = h.digest()
         assert d.live_pages == 0 and d.partition_ok == 1
+
+
+@pytest.mark.parametrize("size", [16, 64, 1000, 8192])
+def test_pattern_passes_cover_every_live_region(cuda, size):
+    """The write/verify passes must touch every byte of every live region (the
+    passes map slots to lanes in strided runs): write seed 1, verify seed 2 ->
+    every 8-byte word of every live region mismatches; verify seed 1 -> none."""
+    torch = cuda
+    n = (1 << 18) + 77  # not a multiple of any run width
+    with ob.Heap(_hc(0, 0, 256 << 20)) as h:
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        h.launch_alloc(n, ptrs, size=size)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        h.launch_count(n, ptrs, cnt)
+        h.launch_write(n, ptrs, 1, 0)
+        good = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
+        h.launch_verify(n, ptrs, 1, 0, good)
+        other = torch.tensor([0, -1, 0, 0], dtype=torch.int64, device="cuda")
+        h.launch_verify(n, ptrs, 2, 0, other)
+        torch.cuda.synchronize()
+        live = int(cnt)
+        page = max(16, 1 << (size - 1).bit_length())
+        assert live > 0
+        assert int(good[0]) == 0
+        assert int(other[0]) == live * (page // 8)
+        h.launch_free(n, ptrs)
+        torch.cuda.synchronize()
+        assert h.last_error()[0] == 0
