@@ -230,7 +230,7 @@ __device__ __forceinline__ void poll_wait() {
 #endif
 }
 __device__ __forceinline__ u64* poll_cache() {
-    __shared__ u64 cache[2 * kPollEntries];  // [0,16) polls, [16,32) hints
+    __shared__ u64 cache[3 * kPollEntries];  // [0,16) polls, [16,32) hints, [32,48) pair polls
     return cache;
 }
 // Queue structs are laid out consecutively, so the struct index is a collision-free
@@ -240,6 +240,12 @@ __device__ __forceinline__ u64 poll_tag(const ouro_queue_dev* Q) {
 }
 __device__ __forceinline__ u64* poll_slot(u64 tag) { return poll_cache() + (tag & 15); }
 __device__ __forceinline__ u64* hint_slot(u64 tag) { return poll_cache() + kPollEntries + (tag & 15); }
+// Chunk-kind retry rounds observe the class queue AND the pool: a pair poll
+// issues both count loads back to back (one L2 round trip, not two) and its
+// entry, keyed by the class queue's tag, holds empty = both empty.  Pair entries
+// are written only by pair polls, so a round never mistakes a class-queue-only
+// observation for one that also covered the pool.
+__device__ __forceinline__ u64* pair_slot(u64 tag) { return poll_cache() + 2 * kPollEntries + (tag & 15); }
 __device__ __forceinline__ bool tag_is(u64 e, u64 tag) { return ((e >> 3) & 31u) == tag; }
 
 // Per-SM hints in HBM (v.sm_hint: 32 entries per SM, hint format): the latest
@@ -269,8 +275,24 @@ __device__ __forceinline__ u32 poll_seq_now(u64 tag) {
 // one in flight, or issues one.
 __device__ __forceinline__ u32 obs_seq(u32 o) { return o >> 1; }
 __device__ __forceinline__ bool obs_empty(u32 o) { return (o & 1u) != 0; }
-__device__ __forceinline__ u32 poll_after_inl(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
-    u64* slot = poll_slot(tag);
+#ifndef OURO_SMH_POLL_PUBLISH
+#define OURO_SMH_POLL_PUBLISH 1
+#endif
+// With P (pair polls, slot = pair_slot): empty = class queue Q empty AND pool P
+// (count - pfloor) empty, both loads issued together.
+__device__ __forceinline__ u32 poll_load(ouro_queue_dev* Q, i64 floor, ouro_queue_dev* P, i64 pfloor, u64 tp,
+                                         u32 now, u64* smh) {
+    if (!P) return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
+    const i64 cq = (i64)ld_rlx((const u64*)&Q->count);
+    const i64 cp = (i64)ld_rlx((const u64*)&P->count);
+    const u32 eq = cq - floor <= 0 ? 1u : 0u, ep = cp - pfloor <= 0 ? 1u : 0u;
+    publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, poll_tag(Q), mk_entry(now, 0, poll_tag(Q), eq));
+    publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tp, mk_entry(now, 0, tp, ep));
+    return eq & ep;
+}
+__device__ __forceinline__ u32 poll_after_inl(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh,
+                                              ouro_queue_dev* P = nullptr, i64 pfloor = 0, u64 tp = 0) {
+    u64* slot = P ? pair_slot(tag) : poll_slot(tag);
     for (int spins = 0; spins < 4096; ++spins) {
         const u32 now = gtime32();
         const u64 e = *reinterpret_cast<volatile u64*>(slot);
@@ -282,16 +304,13 @@ __device__ __forceinline__ u32 poll_after_inl(ouro_queue_dev* Q, i64 floor, u64 
         const u32 ns = (after + 1u) & kSeqMask;
         const u64 fl = mk_entry(now, ns, tag, 2u);
         if (atomicCAS(slot, e, fl) != e) continue;
-        const u32 empty = (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
+        const u32 empty = poll_load(Q, floor, P, pfloor, tp, now, smh);
 
         atomicCAS(slot, fl, mk_entry(now, ns, tag, empty));  // unless a stale-entry reset replaced it
-#ifndef OURO_SMH_POLL_PUBLISH
-#define OURO_SMH_POLL_PUBLISH 1
-#endif
-        publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tag, mk_entry(now, 0, tag, empty));
+        if (!P) publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tag, mk_entry(now, 0, tag, empty));
         return (ns << 1) | empty;
     }
-    return (((after + 1u) & kSeqMask) << 1) | ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u);
+    return (((after + 1u) & kSeqMask) << 1) | poll_load(Q, floor, P, pfloor, tp, gtime32(), smh);
 }
 // Out-of-line form for the one-off callers (first-try hints, pre-checks).
 static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
@@ -317,18 +336,14 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64
 static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
                                                     u32 maxr, u32 policy, u32 base_ns, u32 cap_ns, u64* smh) {
     const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
-    u32 lq = poll_seq_now(tq), lp = P ? poll_seq_now(tp) : 0;  // read after the failed try returned
+    // read after the failed try returned (pair entries: tagged by Q, in their own slots)
+    u32 lq = e_seq(*reinterpret_cast<volatile u64*>(P ? pair_slot(tq) : poll_slot(tq)));
     for (;;) {
         if (++a >= maxr) return (a << 1) | 1u;
         backoff_policy(policy, base_ns, cap_ns, a);
-        const u32 oq = poll_after_inl(Q, 0, tq, lq, smh);
+        const u32 oq = poll_after_inl(Q, 0, tq, lq, smh, P, pfloor, tp);
         lq = obs_seq(oq);
         if (!obs_empty(oq)) break;
-        if (P) {
-            const u32 op = poll_after_inl(P, pfloor, tp, lp, smh);
-            lp = obs_seq(op);
-            if (!obs_empty(op)) break;
-        }
     }
     return a << 1;
 }
@@ -1364,7 +1379,7 @@ __device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, 
 __device__ __forceinline__ void ouro_block_init() {
     const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
-    for (unsigned i = t; i < 2 * ouro_dev::kPollEntries; i += nt) ouro_dev::poll_cache()[i] = 0;
+    for (unsigned i = t; i < 3 * ouro_dev::kPollEntries; i += nt) ouro_dev::poll_cache()[i] = 0;
     __syncthreads();
 }
 // Same, and seed the block's hints from the latest observations other blocks on
@@ -1374,7 +1389,7 @@ __device__ __forceinline__ void ouro_block_init(const ouro_heap_view& h) {
     const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
     u64* cache = poll_cache();
-    for (unsigned i = t; i < 2 * kPollEntries; i += nt) cache[i] = 0;
+    for (unsigned i = t; i < 3 * kPollEntries; i += nt) cache[i] = 0;
     __syncthreads();
     const u64* row = sm_hint_row(h);
     if (row) {
