@@ -333,8 +333,11 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64
 // *attempt counts rounds as the oracle does.  The round loop is ONE out-of-line
 // call with the polls inlined and scalar arguments: a call per round made the
 // caller spill its live state to local memory around every round.
+// PAIR (chunk kind) is a template parameter so the page-kind loop carries no pair-poll code.
+template <bool PAIR>
 static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
                                                     u32 maxr, u32 policy, u32 base_ns, u32 cap_ns, u64* smh) {
+    if (!PAIR) P = nullptr;
     const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
     // read after the failed try returned (pair entries: tagged by Q, in their own slots)
     u32 lq = e_seq(*reinterpret_cast<volatile u64*>(P ? pair_slot(tq) : poll_slot(tq)));
@@ -349,8 +352,10 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
 }
 __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
                                             i64 pfloor, u32* attempt) {
-    const u32 r = fail_rounds_loop(Q, P, pfloor, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
-                                   v.sleep_cap_ns, sm_hint_row(v));
+    const u32 r = P ? fail_rounds_loop<true>(Q, P, pfloor, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
+                                             v.sleep_cap_ns, sm_hint_row(v))
+                    : fail_rounds_loop<false>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
+                                              v.sleep_cap_ns, sm_hint_row(v));
     *attempt = r >> 1;
     return (r & 1u) != 0;
 }
