@@ -334,7 +334,7 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64
 // call with the polls inlined and scalar arguments: a call per round made the
 // caller spill its live state to local memory around every round.
 // PAIR (chunk kind) is a template parameter so the page-kind loop carries no pair-poll code.
-template <bool PAIR>
+template <bool PAIR, bool SLEEP>
 static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
                                                     u32 maxr, u32 policy, u32 base_ns, u32 cap_ns, u64* smh) {
     if (!PAIR) P = nullptr;
@@ -343,7 +343,7 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
     u32 lq = e_seq(*reinterpret_cast<volatile u64*>(P ? pair_slot(tq) : poll_slot(tq)));
     for (;;) {
         if (++a >= maxr) return (a << 1) | 1u;
-        backoff_policy(policy, base_ns, cap_ns, a);
+        backoff_policy(SLEEP ? (u32)OURO_BACKOFF_SLEEP : (u32)OURO_BACKOFF_FENCE, base_ns, cap_ns, a);
         const u32 oq = poll_after_inl(Q, 0, tq, lq, smh, P, pfloor, tp);
         lq = obs_seq(oq);
         if (!obs_empty(oq)) break;
@@ -352,10 +352,15 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
 }
 __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
                                             i64 pfloor, u32* attempt) {
-    const u32 r = P ? fail_rounds_loop<true>(Q, P, pfloor, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
-                                             v.sleep_cap_ns, sm_hint_row(v))
-                    : fail_rounds_loop<false>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff, v.sleep_base_ns,
-                                              v.sleep_cap_ns, sm_hint_row(v));
+    const bool sl = v.backoff == OURO_BACKOFF_SLEEP;
+    const u32 r = P ? (sl ? fail_rounds_loop<true, true>(Q, P, pfloor, *attempt, v.max_retries, v.backoff,
+                                                         v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v))
+                          : fail_rounds_loop<true, false>(Q, P, pfloor, *attempt, v.max_retries, v.backoff,
+                                                          v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v)))
+                    : (sl ? fail_rounds_loop<false, true>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff,
+                                                          v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v))
+                          : fail_rounds_loop<false, false>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff,
+                                                           v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v)));
     *attempt = r >> 1;
     return (r & 1u) != 0;
 }
