@@ -305,6 +305,9 @@ ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s);
 
 const char* ouro_status_name(ouro_status s);
 const char* ouro_build_info(void);
+/* Retry-machinery event counters of an experiment build compiled with
+ * -DOURO_STORM_STATS=1 (all zero in the product build); reset != 0 clears them. */
+ouro_status ouro_debug_counters(uint64_t out[32], int reset);
 
 #ifdef __cplusplus
 }

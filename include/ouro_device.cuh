@@ -181,31 +181,36 @@ __device__ __forceinline__ u32 q_entry(const ouro_heap_view& v, u32 c, u32 gen) 
 }
 
 // ------------------------------------------------------- count / tickets ----
-// Per-block poll combining for retry rounds.  Retrying warps (OOM storms:
-// ~10^6 lanes x max_retries rounds) would otherwise all poll the same count
-// word, and same-address loads serialise in one L2 slice.  Within a block one
-// warp at a time polls a queue's count (CAS marks the entry in flight) and
-// every warp of the block waiting for an observation shares the result.
-// Each retry round needs its OWN observation: poll_after() accepts only a poll
-// issued strictly after the observation the warp's previous round used (for
-// the first round: after its failed try), so OutOfMemory is declared only
-// after max_retries distinct observations of "no page obtainable"
-// -- a queue that refills while a warp retries is seen by its next round.
-// "Issued after" is a per-(block, queue) poll sequence number, not a clock:
-// polls of one entry are issued one at a time and each only after the
-// previous one completed, so a higher sequence number was issued later.  (An
-// ordering by %globaltimer ticks made every round wait for the next 256 ns
-// tick.)
-// Poll entry: [63:32] issue time (globaltimer / 256 ns), [31:8] sequence,
-// [7:3] queue tag, [1] in flight, [0] empty.  Hint entry (first-try hints and
-// pre-checks only, never a round's observation): [63:32] time, [7:3] tag,
-// [0] empty.  Shared memory is not initialised for kernels that do not call
-// ouro_block_init, so an entry counts only if its time lies in
-// [now - window, now + kPollSkew]: garbage that looks like a future entry is
-// rejected.
+// Retry rounds.  An OOM storm is ~10^6 lanes x
+// max_retries rounds, every round needing its OWN observation of the queue's
+// count word -- and same-address loads serialise in one L2 slice.  Within a
+// block the rounds share observations through a "pump": the first warp that
+// needs one becomes the pump and polls the count back to back (one dependent
+// L2 load per round, no shared-memory handshake, no global store on the way),
+// publishing each result with a sequence number in a shared-memory entry; the
+// block's other retrying warps spin on that entry and take the next result.
+// A round accepts only a poll whose sequence is higher than the one its
+// previous round used (for the first round: higher than any poll that may have
+// been in flight when its failed try returned), so OutOfMemory is declared only
+// after max_retries distinct observations, each issued after the previous one
+// completed -- a queue that refills while a warp retries is seen by its next
+// round.  The pump keeps the role across its own rounds and releases it when
+// they end; a waiter that finds no pump takes the role over.  (Measured in
+// isolation, tools/storm_probe.cu mode 5: 2^20 threads x 63 rounds in 98 us;
+// the earlier design -- every round re-acquired the entry by shared CAS,
+// checked %globaltimer windows and published an SM hint to HBM, whose store the
+// next round's fence then waited on -- took 229 us for the same storm.)
+// Observation entry: [63:32] sequence, [7:3] queue tag, [2] pool empty (pair
+// polls), [1] pump active, [0] empty.  Hint entry (first-try hints and
+// pre-checks only, never a round's observation): [63:32] issue time
+// (globaltimer / 256 ns), [7:3] tag, [0] empty.  Shared memory is not
+// initialised for kernels that do not call ouro_block_init, so hints count only
+// if their time lies in [now - window, now + kPollSkew], an entry of another
+// tag is simply taken over, and a pump that makes no progress for kPumpSteal
+// spins is replaced.
 constexpr u32 kPollWindow = 32;  // x 256 ns = 8.2 us
-constexpr u32 kPollSkew = 2;     // entries written just after we read the clock
-constexpr u32 kSeqMask = 0xFFFFFFu;
+constexpr u32 kPollSkew = 2;     // hints written just after we read the clock
+constexpr u32 kPumpSteal = 1u << 12;
 __device__ __forceinline__ u32 gtime32() {
     u64 t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -214,15 +219,37 @@ __device__ __forceinline__ u32 gtime32() {
 __device__ __forceinline__ bool time_recent(u32 now, u64 e, u32 window) {
     return now - (u32)(e >> 32) + kPollSkew < window + kPollSkew;
 }
-__device__ __forceinline__ u32 e_seq(u64 e) { return (u32)(e >> 8) & kSeqMask; }
-__device__ __forceinline__ bool seq_after(u32 a, u32 b) { return ((a - b) & kSeqMask) - 1u < (kSeqMask >> 1); }
-__device__ __forceinline__ u64 mk_entry(u32 now, u32 seq, u64 tag, u32 flags) {
-    return ((u64)now << 32) | ((u64)(seq & kSeqMask) << 8) | (tag << 3) | flags;
+__device__ __forceinline__ u32 e_seq(u64 e) { return (u32)(e >> 32); }
+__device__ __forceinline__ u64 mk_entry(u32 hi, u64 tag, u32 flags) { return ((u64)hi << 32) | (tag << 3) | flags; }
+// Observation entries also carry [31:12] the run of consecutive empty polls ending
+// with this one (saturating): a warp that fell behind its pump can see that every
+// poll it skipped found the queue empty as well.
+constexpr u32 kStreakMax = 0xFFFFFu;
+__device__ __forceinline__ u32 e_streak(u64 e) { return (u32)e >> 12; }
+__device__ __forceinline__ u64 mk_obs(u32 seq, u64 tag, u32 flags, u32 streak) {
+    return mk_entry(seq, tag, flags) | ((u64)(streak < kStreakMax ? streak : kStreakMax) << 12);
 }
+// OURO_STORM_STATS=1: per-SM event counters of the retry machinery (experiment
+// builds only; read with ouro_debug_counters).
+#ifndef OURO_STORM_STATS
+#define OURO_STORM_STATS 0
+#endif
+#if OURO_STORM_STATS
+__device__ unsigned long long g_storm_dbg[256 * 32];
+#define OURO_DBG(i, x) atomicAdd(&g_storm_dbg[(sm_id() & 255u) * 32u + (i)], (unsigned long long)(x))
+struct StormLocal { unsigned long long c[16]; };
+#define OURO_LDBG(L, i, x) ((L) ? (void)((L)->c[i] += (x)) : (void)0)
+#else
+#define OURO_DBG(i, x) ((void)0)
+#define OURO_LDBG(L, i, x) ((void)0)
+struct StormLocal { unsigned long long c[1]; };
+#endif
+constexpr u64 kPump = 2u;
+constexpr u32 kPoolEmpty = 4u;
 constexpr u32 kPollEntries = 16;
-// How a warp waiting for this block's in-flight poll idles between checks.
+// How a warp waiting for its block's pump idles between checks (< 0: spins).
 #ifndef OURO_POLL_WAIT_NS
-#define OURO_POLL_WAIT_NS 32
+#define OURO_POLL_WAIT_NS -1
 #endif
 __device__ __forceinline__ void poll_wait() {
 #if OURO_POLL_WAIT_NS >= 0
@@ -230,7 +257,7 @@ __device__ __forceinline__ void poll_wait() {
 #endif
 }
 __device__ __forceinline__ u64* poll_cache() {
-    __shared__ u64 cache[3 * kPollEntries];  // [0,16) polls, [16,32) hints, [32,48) pair polls
+    __shared__ u64 cache[3 * kPollEntries];  // [0,16) observations, [16,32) hints, [32,48) pair observations
     return cache;
 }
 // Queue structs are laid out consecutively, so the struct index is a collision-free
@@ -243,16 +270,17 @@ __device__ __forceinline__ u64* hint_slot(u64 tag) { return poll_cache() + kPoll
 // Chunk-kind retry rounds observe the class queue AND the pool: a pair poll
 // issues both count loads back to back (one L2 round trip, not two) and its
 // entry, keyed by the class queue's tag, holds empty = both empty.  Pair entries
-// are written only by pair polls, so a round never mistakes a class-queue-only
+// live in their own slots, so a round never mistakes a class-queue-only
 // observation for one that also covered the pool.
 __device__ __forceinline__ u64* pair_slot(u64 tag) { return poll_cache() + 2 * kPollEntries + (tag & 15); }
 __device__ __forceinline__ bool tag_is(u64 e, u64 tag) { return ((e >> 3) & 31u) == tag; }
+__device__ __forceinline__ u64 ld_sh(const u64* p) { return *reinterpret_cast<const volatile u64*>(p); }
 
 // Per-SM hints in HBM (v.sm_hint: 32 entries per SM, hint format): the latest
-// observation any block on this SM made of each queue.  ouro_block_init(v)
+// observation any block on this SM published for each queue.  ouro_block_init(v)
 // seeds a fresh block's hints from them, so the blocks of an OOM storm that
-// start after the queue ran dry make their first try a block-combined poll
-// (one count load per block) instead of an RMW + undo pair per warp.
+// start after the queue ran dry make their first try a block-combined
+// observation instead of an RMW + undo pair per warp.
 __device__ __forceinline__ u64* sm_hint_row(const ouro_heap_view& v) {
     return v.sm_hint ? v.sm_hint + (u64)(sm_id() & 255u) * 32u : nullptr;
 }
@@ -261,121 +289,202 @@ __device__ __forceinline__ void publish_hint(u64* smh, u64 tag, u64 h) {
     if (smh) st_rlx(smh + tag, h);
 }
 
-// The sequence a warp must exceed with its next observation: whatever this
-// block's entry holds now (completed or in flight -- an in-flight poll may have
-// been issued before the caller's failed try).
-__device__ __forceinline__ u32 poll_seq_now(u64 tag) {
-    return e_seq(*reinterpret_cast<volatile u64*>(poll_slot(tag)));
-}
-
-// An observation of (count - floor <= 0) with sequence after `after`.
-// Returns (sequence << 1) | empty -- by value: a result pointer into this
-// __noinline__ function would put the caller's round state in local memory,
-// one L2 write per round.  Reuses a completed poll of this block, waits for
-// one in flight, or issues one.
-__device__ __forceinline__ u32 obs_seq(u32 o) { return o >> 1; }
-__device__ __forceinline__ bool obs_empty(u32 o) { return (o & 1u) != 0; }
-#ifndef OURO_SMH_POLL_PUBLISH
-#define OURO_SMH_POLL_PUBLISH 1
-#endif
-// With P (pair polls, slot = pair_slot): empty = class queue Q empty AND pool P
-// (count - pfloor) empty, both loads issued together.
-__device__ __forceinline__ u32 poll_load(ouro_queue_dev* Q, i64 floor, ouro_queue_dev* P, i64 pfloor, u64 tp,
-                                         u32 now, u64* smh) {
+// One poll: empty = (Q.count - floor <= 0) [and, with P, (P.count - pfloor <= 0)
+// -> bit kPoolEmpty], both loads issued back to back.
+__device__ __forceinline__ u32 poll_load(ouro_queue_dev* Q, i64 floor, ouro_queue_dev* P, i64 pfloor) {
     if (!P) return (i64)ld_rlx((const u64*)&Q->count) - floor <= 0 ? 1u : 0u;
     const i64 cq = (i64)ld_rlx((const u64*)&Q->count);
     const i64 cp = (i64)ld_rlx((const u64*)&P->count);
-    const u32 eq = cq - floor <= 0 ? 1u : 0u, ep = cp - pfloor <= 0 ? 1u : 0u;
-    publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, poll_tag(Q), mk_entry(now, 0, poll_tag(Q), eq));
-    publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tp, mk_entry(now, 0, tp, ep));
-    return eq & ep;
+    const u32 ep = cp - pfloor <= 0 ? 1u : 0u;
+    return ((cq - floor <= 0 ? 1u : 0u) & ep) | (ep ? kPoolEmpty : 0u);
 }
-__device__ __forceinline__ u32 poll_after_inl(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh,
-                                              ouro_queue_dev* P = nullptr, i64 pfloor = 0, u64 tp = 0) {
-    u64* slot = P ? pair_slot(tag) : poll_slot(tag);
-    for (int spins = 0; spins < 4096; ++spins) {
-        const u32 now = gtime32();
-        const u64 e = *reinterpret_cast<volatile u64*>(slot);
-        const bool mine = tag_is(e, tag) && time_recent(now, e, 4 * kPollWindow);
-        if (mine && (e & 2u)) { poll_wait(); continue; }  // in flight: its result or a newer poll
-        if (mine && seq_after(e_seq(e), after)) {
-            return (e_seq(e) << 1) | (u32)(e & 1u);
-        }
-        const u32 ns = (after + 1u) & kSeqMask;
-        const u64 fl = mk_entry(now, ns, tag, 2u);
-        if (atomicCAS(slot, e, fl) != e) continue;
-        const u32 empty = poll_load(Q, floor, P, pfloor, tp, now, smh);
 
-        atomicCAS(slot, fl, mk_entry(now, ns, tag, empty));  // unless a stale-entry reset replaced it
-        if (!P) publish_hint(OURO_SMH_POLL_PUBLISH ? smh : nullptr, tag, mk_entry(now, 0, tag, empty));
-        return (ns << 1) | empty;
+// The lowest sequence the first round after a failed try may use: above the
+// entry's, and above a pump's poll that may have been issued before the try.
+// An entry of another queue (or uninitialised memory) is taken over.
+__device__ __forceinline__ u32 obs_need(u64* slot, u64 tag) {
+    for (;;) {
+        const u64 e = ld_sh(slot);
+        if (tag_is(e, tag)) return e_seq(e) + 1u + (u32)((e & kPump) >> 1);
+        if (atomicCAS(slot, e, mk_entry(0, tag, 0)) == e) return 1u;
     }
-    return (((after + 1u) & kSeqMask) << 1) | poll_load(Q, floor, P, pfloor, tp, gtime32(), smh);
 }
-// Out-of-line form for the one-off callers (first-try hints, pre-checks).
-static __device__ __noinline__ u32 poll_after(ouro_queue_dev* Q, i64 floor, u64 tag, u32 after, u64* smh) {
-    return poll_after_inl(Q, floor, tag, after, smh);
+// One round's observation: a poll with sequence >= *need, taken from this block's
+// pump, or made by this warp when no pump is active (it then becomes the pump:
+// *pumpv holds the entry it wrote, and its next round polls straight away and
+// publishes with a plain store -- waiters only read the entry; a thief that
+// replaced a stalled pump is simply overwritten).  Returns the poll's flag bits
+// (bit 0 = empty).
+__device__ __forceinline__ u32 obs_round(ouro_queue_dev* Q, i64 floor, ouro_queue_dev* P, i64 pfloor, u64* slot,
+                                         u64 tag, u32* need, u64* pumpv, StormLocal* SL = nullptr) {
+    (void)SL;
+    if (*pumpv) {
+        OURO_LDBG(SL, 2, 1);
+        const u32 fl = poll_load(Q, floor, P, pfloor);
+        const u32 s = e_seq(*pumpv) + 1u;
+        const u64 nv = mk_obs(s, tag, (u32)kPump | fl, (fl & 1u) ? e_streak(*pumpv) + 1u : 0u);
+        *reinterpret_cast<volatile u64*>(slot) = nv;
+        *pumpv = nv;
+        *need = s + 1u;
+        return fl;
+    }
+    for (;;) {
+        const u64 e = ld_sh(slot);
+        const bool mine = tag_is(e, tag);
+        if (mine && (int)(e_seq(e) - *need) >= 0) {  // another warp's poll, new enough
+            OURO_LDBG(SL, 3, 1);
+            *need = e_seq(e) + 1u;
+            return (u32)e & (1u | kPoolEmpty);
+        }
+        if (mine && (e & kPump)) {  // wait for the pump's next publication
+            u32 spins = 0;
+            while (ld_sh(slot) == e && ++spins < kPumpSteal) poll_wait();
+            if (spins < kPumpSteal) continue;
+        }
+        // no pump (or it stalled): poll, publish, take the role
+        OURO_LDBG(SL, 2, 1);
+        OURO_LDBG(SL, 4, 1);
+        const u32 fl = poll_load(Q, floor, P, pfloor);
+        const u32 s = mine ? e_seq(e) + 1u : *need;
+        const u64 nv = mk_obs(s, tag, (u32)kPump | fl, (fl & 1u) ? (mine && (e & 1u) ? e_streak(e) + 1u : 1u) : 0u);
+        *pumpv = atomicCAS(slot, e, nv) == e ? nv : 0;  // lost: someone published first; ours stays private
+        OURO_LDBG(SL, 10, *pumpv ? 0 : 1);
+        *need = s + 1u;
+        return fl;
+    }
+}
+__device__ __forceinline__ void obs_release(u64* slot, u64 pumpv) {
+    if (pumpv) atomicCAS(slot, pumpv, pumpv & ~kPump);
+}
+// A single block-combined observation issued after the call (first-try hints,
+// pre-checks): bit 0 = empty.
+static __device__ __noinline__ u32 observe_once(ouro_queue_dev* Q, i64 floor, u64* smh) {
+    OURO_DBG(5, 1);
+    const u64 tag = poll_tag(Q);
+    u64* slot = poll_slot(tag);
+    u32 need = obs_need(slot, tag);
+    u64 pumpv = 0;
+    const u32 fl = obs_round(Q, floor, nullptr, 0, slot, tag, &need, &pumpv);
+    obs_release(slot, pumpv);
+    if (pumpv) publish_hint(smh, tag, mk_entry(gtime32(), tag, fl & 1u));
+    return fl & 1u;
 }
 
 // Pre-check before a reservation RMW (hint: the RMW decides).  One LDS, one
-// clock read when this block has a recent completed observation.
+// clock read when this block has a recent observation.
 __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64* smh) {
     const u64 tag = poll_tag(Q);
-    const u64 h = *reinterpret_cast<volatile u64*>(hint_slot(tag));
+    const u64 h = ld_sh(hint_slot(tag));
     if (tag_is(h, tag) && time_recent(gtime32(), h, kPollWindow)) return (h & 1u) != 0;
-    return obs_empty(poll_after(Q, floor, tag, poll_seq_now(tag), smh));
+    return observe_once(Q, floor, smh) != 0;
 }
 
-// Failed retry rounds on a group leader: backoff, then a
-// block-combined observation of the class queue (and, for the chunk kind, of
-// the pool) newer than the previous round's; stops when one sees work
-// (returns false) or when the budget is spent (returns true: OutOfMemory).
-// *attempt counts rounds as the oracle does.  The round loop is ONE out-of-line
-// call with the polls inlined and scalar arguments: a call per round made the
-// caller spill its live state to local memory around every round.
-// PAIR (chunk kind) is a template parameter so the page-kind loop carries no pair-poll code.
+// Failed retry rounds on a group leader: backoff, then an
+// observation of the class queue (and, for the chunk kind, of the pool) newer than
+// the previous round's; stops when one sees work (returns false) or when the
+// budget is spent (returns true: OutOfMemory).  *attempt counts rounds as the
+// oracle does.  The round loop is ONE out-of-line call with the polls inlined and
+// scalar arguments: a call per round made the caller spill its live state to
+// local memory around every round.  PAIR (chunk kind) and SLEEP (backoff policy)
+// are template parameters so each loop carries only its own code.
+#ifndef OURO_PUMP_UNROLL
+#define OURO_PUMP_UNROLL 16
+#endif
+constexpr int kPumpUnroll = OURO_PUMP_UNROLL;
 template <bool PAIR, bool SLEEP>
 static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
-                                                    u32 maxr, u32 policy, u32 base_ns, u32 cap_ns, u64* smh) {
+                                                    u32 maxr, u32 base_ns, u32 cap_ns, u64* smh) {
     if (!PAIR) P = nullptr;
-    const u64 tq = poll_tag(Q), tp = P ? poll_tag(P) : 0;
-    // read after the failed try returned (pair entries: tagged by Q, in their own slots)
-    u32 lq = e_seq(*reinterpret_cast<volatile u64*>(P ? pair_slot(tq) : poll_slot(tq)));
+    const u64 tag = poll_tag(Q);
+    u64* slot = PAIR ? pair_slot(tag) : poll_slot(tag);
+    u32 need = obs_need(slot, tag), fl = 1u, seq = 0, streak = 0, extra = 0;
+    // Waiting rounds: take the pump's polls, or claim the role when there is no pump.
     for (;;) {
         if (++a >= maxr) return (a << 1) | 1u;
         backoff_policy(SLEEP ? (u32)OURO_BACKOFF_SLEEP : (u32)OURO_BACKOFF_FENCE, base_ns, cap_ns, a);
-        const u32 oq = poll_after_inl(Q, 0, tq, lq, smh, P, pfloor, tp);
-        lq = obs_seq(oq);
-        if (!obs_empty(oq)) break;
+        // FenceRetry: a round may take a poll the pump made while this warp was
+        // still on an earlier round -- each such poll is newer than the previous
+        // round's and found the queue empty (streak), so it is this round's
+        // observation.  (SleepRetry keeps one poll per round: its sleeps pace it.)
+        if (!SLEEP && extra) { --extra; continue; }
+        bool claimed = false;
+        for (u32 spins = 0;;) {
+            const u64 e = ld_sh(slot);
+            const bool mine = tag_is(e, tag);
+            if (mine && (int)(e_seq(e) - need) >= 0) {  // the pump's poll, new enough
+                fl = (u32)e & (1u | kPoolEmpty);
+                const u32 avail = e_seq(e) - need;       // older polls this warp skipped
+                if (!SLEEP && (fl & 1u) && e_streak(e) > avail) extra = avail;
+                need = e_seq(e) + 1u;
+                break;
+            }
+            if (!(mine && (e & kPump) && ++spins < kPumpSteal)) {
+                // no pump (or it stalled): claim the role; this round's poll is ours
+                seq = mine ? e_seq(e) : need - 1u;
+                streak = mine && (e & 1u) ? e_streak(e) : 0u;
+                if (atomicCAS(slot, e, mk_obs(seq, tag, (u32)kPump, streak)) == e) { claimed = true; break; }
+                spins = 0;
+            }
+            poll_wait();
+        }
+        if (claimed) break;
+        if (!(fl & 1u)) return a << 1;
     }
-    return a << 1;
+    // Pump rounds: poll back to back (this round's poll first).  Unrolled: ptxas
+    // puts a YIELD at the head of a loop whose exit depends on a loaded value, and
+    // a yield per round cost the pump ~350 cycles with the SM's other warps ready
+    // (tools/rounds_probe.cu: 127 -> 78 us for 2^20 threads x 62 rounds).
+    u32 r;
+    bool first = true;
+#pragma unroll kPumpUnroll
+    for (;;) {
+        if (!first) {
+            if (++a >= maxr) { r = (a << 1) | 1u; break; }
+            backoff_policy(SLEEP ? (u32)OURO_BACKOFF_SLEEP : (u32)OURO_BACKOFF_FENCE, base_ns, cap_ns, a);
+        }
+        first = false;
+        fl = poll_load(Q, 0, P, pfloor);
+        ++seq;
+        streak = (fl & 1u) ? streak + 1u : 0u;
+        *reinterpret_cast<volatile u64*>(slot) = mk_obs(seq, tag, (u32)kPump | fl, streak);
+        if (!(fl & 1u)) { r = a << 1; break; }
+    }
+    *reinterpret_cast<volatile u64*>(slot) = mk_obs(seq, tag, fl, streak);  // release: the last poll stays readable
+    // seed the hints of blocks that start later on this SM (one store per pump term)
+    if (PAIR) publish_hint(smh, poll_tag(P), mk_entry(gtime32(), poll_tag(P), (fl & kPoolEmpty) ? 1u : 0u));
+    else publish_hint(smh, tag, mk_entry(gtime32(), tag, fl & 1u));
+    return r;
 }
 __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_dev* Q, ouro_queue_dev* P,
                                             i64 pfloor, u32* attempt) {
     const bool sl = v.backoff == OURO_BACKOFF_SLEEP;
-    const u32 r = P ? (sl ? fail_rounds_loop<true, true>(Q, P, pfloor, *attempt, v.max_retries, v.backoff,
-                                                         v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v))
-                          : fail_rounds_loop<true, false>(Q, P, pfloor, *attempt, v.max_retries, v.backoff,
-                                                          v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v)))
-                    : (sl ? fail_rounds_loop<false, true>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff,
-                                                          v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v))
-                          : fail_rounds_loop<false, false>(Q, nullptr, 0, *attempt, v.max_retries, v.backoff,
-                                                           v.sleep_base_ns, v.sleep_cap_ns, sm_hint_row(v)));
+    u64* smh = sm_hint_row(v);
+    const u32 r = P ? (sl ? fail_rounds_loop<true, true>(Q, P, pfloor, *attempt, v.max_retries, v.sleep_base_ns,
+                                                         v.sleep_cap_ns, smh)
+                          : fail_rounds_loop<true, false>(Q, P, pfloor, *attempt, v.max_retries, v.sleep_base_ns,
+                                                          v.sleep_cap_ns, smh))
+                    : (sl ? fail_rounds_loop<false, true>(Q, nullptr, 0, *attempt, v.max_retries, v.sleep_base_ns,
+                                                          v.sleep_cap_ns, smh)
+                          : fail_rounds_loop<false, false>(Q, nullptr, 0, *attempt, v.max_retries, v.sleep_base_ns,
+                                                           v.sleep_cap_ns, smh));
     *attempt = r >> 1;
     return (r & 1u) != 0;
 }
 
 // Did this block recently see the queue empty?  (hint only: it just turns the
-// first try's RMW into load-then-RMW, which reserves exactly the same.)
+// first try's RMW into observe-then-RMW, which reserves exactly the same.)  A
+// pump active in this block is the freshest evidence.
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
-    const u64 e = *reinterpret_cast<volatile u64*>(hint_slot(tag));
+    const u64 o = ld_sh(poll_slot(tag));
+    if (tag_is(o, tag) && (o & kPump)) return (o & 1u) != 0;
+    const u64 e = ld_sh(hint_slot(tag));
     return tag_is(e, tag) && (e & 1u) && time_recent(gtime32(), e, 4 * kPollWindow);
 }
 // A reservation RMW issued at tick t0 found the queue empty: record the hint.
 __device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u32 t0, u64* smh) {
     const u64 tag = poll_tag(Q);
-    publish_hint(smh, tag, mk_entry(t0, 0, tag, 1u));
+    publish_hint(smh, tag, mk_entry(t0, tag, 1u));
 }
 
 // Count reservation (broker-queue style).
@@ -396,10 +505,10 @@ __device__ __forceinline__ u32 reserve_deq(const ouro_heap_view& v, ouro_queue_d
             return 0;
         }
     } else if (hint_empty(Q)) {
-        const u64 tag = poll_tag(Q);
-        if (obs_empty(poll_after(Q, floor, tag, poll_seq_now(tag), sm_hint_row(v)))) return 0;
+        if (observe_once(Q, floor, sm_hint_row(v))) return 0;
     }
     const u32 t0 = gtime32();
+    OURO_DBG(7, 1);
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)(-(i64)n));
     const i64 avail = old - floor;
     const u32 got = avail <= 0 ? 0u : (avail >= (i64)n ? n : (u32)avail);
@@ -1056,6 +1165,10 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     const u32 lt = lanemask_lt();
     const u32 gl0 = __ffs(gm) - 1;
     u64 retries = 0;
+#if OURO_STORM_STATS
+    const u64 tp0 = clock64();
+    u64 tp1 = 0, tp2 = 0;
+#endif
     while (todo) {
         const u32 rank = __popc(todo & lt);
         u32 h = NONE;
@@ -1100,7 +1213,13 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         // oracle's (one failed try per round, OOM after max_retries).
         const u32 leader = __ffs(todo) - 1, rem = __popc(todo);
         u32 a = attempt, oom = 0;
+#if OURO_STORM_STATS
+        if (!tp1) tp1 = clock64();
+#endif
         if (lane == leader) oom = fail_rounds(v, v.q + k, nullptr, 0, &a) ? 1u : 0u;
+#if OURO_STORM_STATS
+        tp2 = clock64();
+#endif
         a = __shfl_sync(mask, a, leader);
         oom = __shfl_sync(mask, oom, leader);
         retries += (u64)rem * (a - attempt);
@@ -1112,6 +1231,14 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         }
     }
     if (retries && lane == gl0) atomicAdd(ctr_at(v, k), retries);  // one update per call, not per round
+#if OURO_STORM_STATS
+    if (lane == gl0 && tp1) {
+        OURO_DBG(16, 1);
+        OURO_DBG(17, tp1 - tp0);
+        OURO_DBG(18, tp2 - tp1);
+        OURO_DBG(19, clock64() - tp2);
+    }
+#endif
 }
 
 // Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).

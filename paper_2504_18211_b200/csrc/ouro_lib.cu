@@ -137,12 +137,26 @@ __global__ void k_init_pq_chunks(ouro_heap_view v, const u32* pq) {
 #endif
 template <int KIND, int FL, class SZ = u32>
 __global__ void __launch_bounds__(kBlock, OURO_ALLOC_MIN_BLOCKS) k_alloc(ouro_heap_view v, u64 n, u64 uniform, const SZ* sizes, void** out) {
+#if OURO_STORM_STATS
+    const u64 tk0 = clock64();
+#endif
     ouro_block_init(v);
+#if OURO_STORM_STATS
+    const u64 tk1 = clock64();
+#endif
     const u64 stride = (u64)gridDim.x * blockDim.x;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i - threadIdx.x % 32 < n; i += stride) {
         const u32 lanes = __ballot_sync(0xFFFFFFFFu, i < n);
         if (i < n) out[i] = ouro_malloc_t<KIND, FL>(v, sizes ? sizes[i] : uniform, nullptr, lanes);
     }
+#if OURO_STORM_STATS
+    if ((threadIdx.x & 31) == 0) {
+        OURO_DBG(20, 1);
+        OURO_DBG(21, tk1 - tk0);
+        OURO_DBG(22, clock64() - tk1);
+        if (threadIdx.x == 0) { OURO_DBG(23, 1); u64 g; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g)); OURO_DBG(24, g >> 10); }
+    }
+#endif
 }
 template <int KIND, int FL>
 __global__ void __launch_bounds__(kBlock) k_free(ouro_heap_view v, u64 n, void* const* ptrs) {
@@ -1323,6 +1337,23 @@ ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     cudaFree(buf);
+    return OURO_OK;
+}
+
+// Event counters of an OURO_STORM_STATS=1 experiment build (zeros otherwise).
+ouro_status ouro_debug_counters(uint64_t out[32], int reset) {
+    std::memset(out, 0, 32 * 8);
+#if OURO_STORM_STATS
+    std::vector<u64> h(256 * 32);
+    CK(cudaMemcpyFromSymbol(h.data(), g_storm_dbg, h.size() * 8));
+    for (size_t i = 0; i < h.size(); ++i) out[i % 32] += h[i];
+    if (reset) {
+        std::fill(h.begin(), h.end(), 0ull);
+        CK(cudaMemcpyToSymbol(g_storm_dbg, h.data(), h.size() * 8));
+    }
+#else
+    (void)reset;
+#endif
     return OURO_OK;
 }
 

@@ -42,6 +42,41 @@ struct St {
     u64 rep[256 * kStride];
 };
 
+// mode 6 body: lane 0 alone, out of line, the other lanes parked (the allocator's shape)
+static __device__ __noinline__ u64 pump_rounds(St* s, u64* ent, int rounds, int sleep_ns) {
+    volatile u64* ve = ent;
+    bool pump = false;
+    u64 last = 0, acc = 0;
+    { const u64 e0 = *ve; last = (e0 >> 2) + ((e0 >> 1) & 1); }
+    for (int r = 0; r < rounds; ++r) {
+        asm volatile("fence.sc.cta;" ::: "memory");
+        if (pump) {
+            const u64 c = ld_rlx(&s->count);
+            ++last;
+            *ve = (last << 2) | 2u | (c == 0 ? 1u : 0u);
+            acc += c;
+        } else {
+            for (;;) {
+                const u64 e = *ve;
+                if ((e >> 2) > last) { last = e >> 2; break; }
+                if (!(e & 2u)) {
+                    if (atomicCAS(ent, e, e | 2u) == e) {
+                        pump = true;
+                        const u64 c = ld_rlx(&s->count);
+                        last = (e >> 2) + 1;
+                        *ve = (last << 2) | 2u | (c == 0 ? 1u : 0u);
+                        break;
+                    }
+                    continue;
+                }
+                if (sleep_ns) __nanosleep(sleep_ns);
+            }
+        }
+    }
+    if (pump) *ve = (last << 2) | (*ve & 1u);
+    return acc;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256, 6) k_storm(St* s, int rounds, int R, int sleep_ns) {
     const u32 lane = threadIdx.x & 31;
@@ -53,6 +88,16 @@ __global__ void __launch_bounds__(256, 6) k_storm(St* s, int rounds, int R, int 
             acc = __shfl_sync(0xFFFFFFFFu, acc, 0);
         }
         if (acc == 12345) s->stats[3] = acc;
+        return;
+    }
+    if (MODE == 6) {
+        __shared__ u64 ent6;
+        if (threadIdx.x == 0) ent6 = 0;
+        __syncthreads();
+        u64 acc = 0;
+        if (lane == 0) acc = pump_rounds(s, &ent6, rounds, sleep_ns);
+        acc = __shfl_sync(0xFFFFFFFFu, acc, 0);
+        if (acc == 12345) s->stats[5] = acc;
         return;
     }
     if (MODE == 5) {
@@ -201,18 +246,20 @@ int main(int argc, char** argv) {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     unsigned nb = blocks, nt = threads;
+    int smem = 0;  // dynamic shared memory: 36 KiB forces 6 blocks/SM like k_alloc
     auto run = [&](int mode, int R, int sl) {
         float best = 1e30f;
         u64 st[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int it = 0; it < 5; ++it) {
             cudaMemset(s, 0, sizeof(St));
             cudaEventRecord(a);
-            if (mode == 0) k_storm<0><<<nb, nt>>>(s, rounds, R, sl);
-            else if (mode == 1) k_storm<1><<<nb, nt>>>(s, rounds, R, sl);
-            else if (mode == 2) k_storm<2><<<nb, nt>>>(s, rounds, R, sl);
-            else if (mode == 3) k_storm<3><<<nb, nt>>>(s, rounds, R, sl);
-            else if (mode == 4) k_storm<4><<<nb, nt>>>(s, rounds, R, sl);
-            else k_storm<5><<<nb, nt>>>(s, rounds, R, sl);
+            if (mode == 0) k_storm<0><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else if (mode == 1) k_storm<1><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else if (mode == 2) k_storm<2><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else if (mode == 3) k_storm<3><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else if (mode == 4) k_storm<4><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else if (mode == 5) k_storm<5><<<nb, nt, smem>>>(s, rounds, R, sl);
+            else k_storm<6><<<nb, nt, smem>>>(s, rounds, R, sl);
             cudaEventRecord(b);
             cudaEventSynchronize(b);
             float ms;
@@ -221,15 +268,16 @@ int main(int argc, char** argv) {
             cudaMemcpy(st, s->stats, 64, cudaMemcpyDeviceToHost);
         }
         cudaError_t e = cudaGetLastError();
-        printf("[%u x %u] mode %d R %3d sleep %4d: %8.1f us  terms %llu polls %llu  count-load %llu cyc  obs-iter %llu cyc  "
-               "spins/round %.2f %s\n", nb, nt, mode, R, sl, best * 1e3, st[0], st[1], st[1] ? st[2] / st[1] : 0ull,
+        printf("[smem %d] [%u x %u] mode %d R %3d sleep %4d: %8.1f us  terms %llu polls %llu  count-load %llu cyc  obs-iter %llu cyc  "
+               "spins/round %.2f %s\n", smem, nb, nt, mode, R, sl, best * 1e3, st[0], st[1], st[1] ? st[2] / st[1] : 0ull,
                st[1] ? st[3] / st[1] : 0ull, st[4] / (64.0 * 63.0), e == cudaSuccess ? "" : cudaGetErrorString(e));
     };
     run(0, 1, 0);
     for (int R : {32, 64, 148}) run(1, R, 0);
     run(2, 64, 0);
-    run(5, 1, 0); run(5, 1, 32); run(5, 1, 64); run(5, 1, 128);
-    nb = 1; nt = 32; run(5, 1, 0);
-    nb = 888; nt = 256; run(5, 1, 32);
+    run(6, 1, 0); run(6, 1, 64);
+    cudaFuncSetAttribute(k_storm<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 36 << 10);
+    smem = 36 << 10;
+    run(6, 1, 0); run(6, 1, 64);
     return 0;
 }
