@@ -1160,6 +1160,8 @@ namespace {
 template <class F>
 void for_each_queued(orc_heap* h, Queue& Q, F f) {
     Arena& ar = h->ar;
+    // VirtualList: one walk along the list as the tickets advance (segment order)
+    u32 cur = (u32)Q.vl_head, i = (u32)(Q.vl_head >> 32);
     for (u64 t = Q.head; t < Q.tail; ++t) {
         u64 x;
         if (Q.flavor == OURO_FLAVOR_ARRAY) {
@@ -1171,13 +1173,9 @@ void for_each_queued(orc_heap* h, Queue& Q, F f) {
             x = ar.cw((u32)e)[t % ar.S_va()];
         } else {
             const u64 s = t / ar.S_vl();
-            u32 cur = (u32)Q.vl_head;
-            u32 i = (u32)(Q.vl_head >> 32);
-            if (cur == NONE) continue;
-            while (i != (u32)s) {
+            while (cur != NONE && i != (u32)s) {
                 const u64 nx = ar.cw(cur)[0];
-                if (nx == NONE_LINK) { cur = NONE; break; }
-                cur = (u32)nx;
+                cur = nx == NONE_LINK ? NONE : (u32)nx;
                 ++i;
             }
             if (cur == NONE) continue;
@@ -1662,6 +1660,39 @@ ouro_status orc_churn(orc_heap* h, uint64_t n, uint32_t round_begin, uint32_t ro
     out->mallocs_failed = mbad;
     out->frees = fr;
     out->check_failures = chk;
+    return OURO_OK;
+}
+
+// The GPU driver phases' demand on the oracle: n slots in warp groups of `group`
+// lanes, slot order, one thread (deterministic).  Slot i requests sizes[i] (or
+// `bytes`); out[i] = heap offset or ~0 on failure.  Returns the success count.
+ouro_status orc_alloc_slots(orc_heap* h, uint64_t n, uint64_t bytes, const uint32_t* sizes, uint32_t group,
+                            uint64_t* out, uint64_t* ok) {
+    if (group == 0 || group > 64) return OURO_ERR_USAGE;
+    std::vector<Lane> L(group);
+    u64 good = 0;
+    for (u64 i = 0; i < n; i += group) {
+        const u32 m = (u32)std::min<u64>(group, n - i);
+        for (u32 j = 0; j < m; ++j) { L[j] = Lane{}; L[j].off = sizes ? sizes[i + j] : bytes; }
+        h->alloc_group(L.data(), m);
+        for (u32 j = 0; j < m; ++j) {
+            out[i + j] = L[j].st == OURO_OK ? L[j].off : ~0ull;
+            good += L[j].st == OURO_OK;
+        }
+    }
+    if (ok) *ok = good;
+    return OURO_OK;
+}
+// Free the non-~0 offsets of n slots in warp groups of `group` lanes (slot order).
+ouro_status orc_free_slots(orc_heap* h, uint64_t n, const uint64_t* offs, uint32_t group) {
+    if (group == 0 || group > 64) return OURO_ERR_USAGE;
+    std::vector<Lane> L(group);
+    for (u64 i = 0; i < n; i += group) {
+        u32 m = 0;
+        for (u64 j = i; j < std::min<u64>(i + group, n); ++j)
+            if (offs[j] != ~0ull) { L[m] = Lane{}; L[m].off = offs[j]; ++m; }
+        if (m) h->free_group(L.data(), m);
+    }
     return OURO_OK;
 }
 

@@ -103,6 +103,11 @@ ouro_status orc_churn(orc_heap* h, uint64_t n, uint32_t round_begin, uint32_t ro
                       double* ms);
 /* Free every non-~0 offset in slots (single thread, slot order) and reset them. */
 ouro_status orc_free_all(orc_heap* h, uint64_t n, uint64_t* slots);
+/* n slots in warp groups of `group` lanes in slot order, one thread (the demand
+ * of the GPU driver phases); out[i] = offset or ~0; *ok = successes. */
+ouro_status orc_alloc_slots(orc_heap* h, uint64_t n, uint64_t bytes, const uint32_t* sizes, uint32_t group,
+                            uint64_t* out, uint64_t* ok);
+ouro_status orc_free_slots(orc_heap* h, uint64_t n, const uint64_t* offs, uint32_t group);
 
 #ifdef __cplusplus
 }

@@ -77,6 +77,8 @@ def oracle():
             "orc_churn": (i32, [P, u64, u32, u32, u64, u32, C.POINTER(u64), C.POINTER(ChurnResult),
                                 C.POINTER(C.c_double)]),
             "orc_free_all": (i32, [P, u64, C.POINTER(u64)]),
+            "orc_alloc_slots": (i32, [P, u64, u64, C.POINTER(u32), u32, C.POINTER(u64), C.POINTER(u64)]),
+            "orc_free_slots": (i32, [P, u64, C.POINTER(u64), u32]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -154,6 +156,30 @@ class OHeap:
         st = (C.c_int32 * n)()
         assert self.L.orc_alloc_coalesced(self.h, n, nbytes, off, st) == 0
         return list(off), list(st)
+
+    def alloc_slots(self, n, nbytes=0, sizes=None, group=32):
+        """n slots in warp groups (slot order): (offsets array, success count)."""
+        out = (C.c_uint64 * n)()
+        ok = C.c_uint64()
+        sz = None
+        if sizes is not None:
+            sz = (C.c_uint32 * n)(*sizes)
+        assert self.L.orc_alloc_slots(self.h, n, nbytes, sz, group, out, C.byref(ok)) == 0
+        return out, ok.value
+
+    def free_slots(self, offs, group=32):
+        assert self.L.orc_free_slots(self.h, len(offs), offs, group) == 0
+
+    def churn(self, n, round_begin, rounds, seed, threads=1, slots=None):
+        """orc_churn over n slots; returns (slots array, ChurnResult)."""
+        if slots is None:
+            slots = (C.c_uint64 * n)(*([2 ** 64 - 1] * n))
+        res, ms = ChurnResult(), C.c_double()
+        assert self.L.orc_churn(self.h, n, round_begin, rounds, seed, threads, slots, C.byref(res), C.byref(ms)) == 0
+        return slots, res
+
+    def free_all(self, slots):
+        assert self.L.orc_free_all(self.h, len(slots), slots) == 0
 
     def run_script(self, steps):
         arr = make_steps(steps)

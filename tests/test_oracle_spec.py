@@ -377,3 +377,37 @@ def test_concurrency_churn_no_duplicates(variant):
     d = h.digest()
     assert d.live_pages == 0 and d.partition_ok == 1
     h.close()
+
+
+def test_alloc_slots_page_capacities():
+    """orc_alloc_slots (the oracle side of tests/test_gpu_baseline.py): on the BASELINE
+    configs[1] heap the page kind serves min(n, capacity) of 2^20 requests, capacity =
+    1638 chunks x pages per chunk above the 64 B class, and a free-all
+    restores the initial digest."""
+    h = OHeap(cfg(0, 0, 1 << 30, retries=4))
+    d0 = h.digest().as_dict()
+    n = 1 << 20
+    for size, want in ((16, n), (128, 1638 * 512), (8192, 1638 * 8)):
+        offs, ok = h.alloc_slots(n, size)
+        assert ok == want
+        assert sum(1 for x in offs if x != 2 ** 64 - 1) == ok
+        h.free_slots(offs)
+        assert h.digest().as_dict() == d0
+    h.close()
+
+
+@pytest.mark.parametrize("flavor", [0, 1, 2])
+def test_churn_digest_independent_of_threads(flavor):
+    """The chunk kind's free-all state after churn does not depend on the interleaving
+    (one thread vs eight): the property the GPU churn parity test relies on."""
+    digests, counts = [], []
+    for threads in (1, 8):
+        h = OHeap(cfg(1, flavor, 64 << 20))
+        slots, res = h.churn(8192, 0, 10, 5, threads=threads)
+        assert res.mallocs_failed == 0 and res.check_failures == 0
+        counts.append((res.mallocs_ok, res.frees))
+        h.free_all(slots)
+        digests.append(h.digest().as_dict())
+        h.close()
+    assert counts[0] == counts[1]
+    assert digests[0] == digests[1]
