@@ -133,20 +133,76 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ reference ----
-def run_reference(args, cfgname):
-    """The reference CPU allocator: the SPEC-faithful oracle restatement
-    (oracle/ouro_oracle.cpp; the reference tree has no runnable allocator),
-    on all host threads, one bounded sample of the same workload per step."""
+def _metric():
+    """BASELINE.json's metric string, identical in both arms."""
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "malloc+free ops/sec vs size (16 B\u20138 KiB, 1M threads); % of L2-atomic roofline"
+
+
+def config_dict(cfgname, hc_variant=None):
+    """The `config` object both arms print for a sweep configuration."""
+    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    from paper_2504_18211_b200._abi import variant_name_of
+    return {"workload": desc, "variant": variant_name_of(kind, flavor), "heap_bytes": heap, "threads": n,
+            "sizes": sizes, "unit_of_work": "one successful malloc+free pair",
+            "value_formula": "sum over sizes of successful pairs / sum over sizes of (alloc + free time)",
+            "backoff": "FenceRetry, fence.sc.cta between rounds (SPEC.md:279 asks seq-cst; CTA scope is the "
+                       "documented deviation, DESIGN.md section 3), max_retries 64"}
+
+
+def cpu_sweep(cfgname, passes, warmup, threads):
+    """The reference CPU allocator (the SPEC restatement oracle/ouro_oracle.cpp on
+    std::thread workers behind a start barrier, SPEC.md:379-387, 418) on the SAME
+    workload as the GPU arm: 2^20 slots per size, the same sizes, one persistent
+    heap.  A pass = one size's trial of 2 iterations (alloc all / write / verify /
+    free all); its timed figure is iteration 2 (mean_subsequent).
+    Passes cycle through the sizes; every size gets >= 1 timed pass.  Returns the
+    per-size means and value = sum of per-size pairs / sum of per-size times, the
+    GPU arm's composition."""
     from oracle_lib import OHeap, TrialOut, oracle
     from paper_2504_18211_b200._abi import Config
     desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
-    threads = args.ref_threads or os.cpu_count() or 1
-    sample = min(n, 1 << 17)
     cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
     L = oracle()
     oh = OHeap(cfg)
+    per = {s: {"ok": [], "ms": []} for s in sizes}
+    timed = max(passes, len(sizes))
+    verified = True
+    pass_ms = []
+    for i in range(warmup + timed):
+        s = sizes[i % len(sizes)]
+        out = TrialOut()
+        assert L.orc_bench_trial(oh.h, n, s, None, 2, threads, 7, C.byref(out)) == 0
+        verified = verified and bool(out.verified)
+        if i >= warmup:
+            per[s]["ok"].append(out.ok_allocs // 2)
+            per[s]["ms"].append(out.alloc_ms[1] + out.free_ms[1])
+            pass_ms.append(out.alloc_ms[1] + out.free_ms[1])
+    oh.close()
+    ok = sum(statistics.mean(p["ok"]) for p in per.values())
+    ms = sum(statistics.mean(p["ms"]) for p in per.values())
+    per_size = {str(s): {"ok": int(statistics.mean(p["ok"])), "alloc_free_ms": round(statistics.mean(p["ms"]), 3),
+                         "passes": len(p["ms"])} for s, p in per.items()}
+    return {"value": ok / (ms / 1e3), "per_size": per_size, "ms_per_step": statistics.mean(pass_ms),
+            "timed_passes": timed, "verified": verified, "threads": threads, "slots": n}
+
+
+def run_reference(args, cfgname):
+    """--impl reference: the reference CPU allocator on all host threads, same
+    metric / unit / config as the GPU arm (the reference tree has no runnable
+    allocator, so its CPU restatement is the reference)."""
+    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    threads = args.ref_threads or os.cpu_count() or 1
     if sizes is None:  # churn: ops = mallocs + frees per second
-        from paper_2504_18211_b200._abi import ChurnResult
+        from oracle_lib import OHeap, oracle
+        from paper_2504_18211_b200._abi import ChurnResult, Config
+        sample = min(n, 1 << 20)
+        cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
+        L = oracle()
+        oh = OHeap(cfg)
         slots = (C.c_uint64 * sample)(*([2 ** 64 - 1] * sample))
         tot_ops, tot_s, r0 = 0, 0.0, 0
         for step in range(args.warmup + args.steps):
@@ -168,63 +224,33 @@ def run_reference(args, cfgname):
                              "sample": f"{sample} slots x {CHURN_ROUNDS_PER_STEP} rounds per step"},
             "e2e": {"value": value, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
-
-    def one_step():
-        ok = 0
-        secs = 0.0
-        for s in sizes:
-            out = TrialOut()
-            assert L.orc_bench_trial(oh.h, sample, s, None, 1, threads, 7, C.byref(out)) == 0
-            ok += out.ok_allocs
-            secs += (out.alloc_ms[0] + out.free_ms[0]) / 1e3
-        return ok, secs
-
-    for _ in range(args.warmup):
-        one_step()
-    tot_ok, tot_s = 0, 0.0
-    for _ in range(args.steps):
-        ok, s = one_step()
-        tot_ok += ok
-        tot_s += s
-    value = tot_ok / tot_s
+    r = cpu_sweep(cfgname, args.steps, args.warmup, threads)
+    sample = (f"{n} slots per size (the GPU arm's thread count), sizes {sizes}; a step = one size's trial "
+              f"of 2 iterations timed on iteration 2 (mean_subsequent), sizes cycled, {r['timed_passes']} timed "
+              f"steps after {args.warmup} warm-up steps; oracle/ouro_oracle.cpp on std::thread x {threads}")
     line = {
-        "metric": "malloc+free pairs/s (successful), size sweep",
-        "impl": "reference", "value": value, "unit": "pairs/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "metric": _metric(), "impl": "reference", "value": r["value"], "unit": "pairs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["ms_per_step"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32/u64",
-        "data": "synthetic", "config": {"workload": desc, "sample_threads_per_size": sample,
-                                        "sizes": sizes},
-        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
-                         "sample": f"{sample} slots per size x {len(sizes)} sizes per step (oracle/ouro_oracle.cpp)"},
-        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic", "same_config": True,
+        "config": dict(config_dict(cfgname), per_size=r["per_size"], verified=r["verified"]),
+        "cpu_baseline": {"value": r["value"], "unit": "pairs/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": r["value"], "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
 def cpu_baseline(cfgname):
-    """Oracle port timed on the host cores: 2^20 slots x malloc(16) / free,
-    second iteration (mean_subsequent)."""
-    from oracle_lib import OHeap, TrialOut, oracle
-    from paper_2504_18211_b200._abi import Config
-    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    """The reference CPU allocator timed beside the GPU arm (rank 0, N=1): the same
+    sweep as the reference arm, one timed pass per size after no warm-up step (each
+    pass is itself a 2-iteration trial timed on iteration 2)."""
     threads = os.cpu_count() or 1
-    cfg = Config(heap, 64 << 10, 16, 8192, flavor, kind, 0, 0, 64, 100, 100000)
-    oh = OHeap(cfg)
-    size = 16
-    ok, secs, iters, verified = 0, 0.0, 0, True
-    t_end = time.perf_counter() + 10.0      # ~10 s of CPU work
-    while time.perf_counter() < t_end and iters < 200:
-        out = TrialOut()
-        assert oracle().orc_bench_trial(oh.h, n, size, None, 4, threads, 7, C.byref(out)) == 0
-        for i in range(1, 4):               # mean_subsequent: first iteration of each trial excluded
-            secs += (out.alloc_ms[i] + out.free_ms[i]) / 1e3
-        ok += out.ok_allocs * 3 // 4
-        iters += 3
-        verified = verified and bool(out.verified)
-    oh.close()
-    return {"value": ok / secs, "unit": "pairs/s", "cores": threads, "kind": "port",
-            "sample": f"{n} slots x malloc({size})/free, {iters} timed iterations (~10 s), "
-                      f"oracle/ouro_oracle.cpp on std::thread x {threads}", "verified": verified}
+    r = cpu_sweep(cfgname, 0, 0, threads)
+    desc, kind, flavor, heap, n, sizes = CONFIGS[cfgname]
+    return {"value": r["value"], "unit": "pairs/s", "cores": threads, "kind": "port",
+            "sample": f"{n} slots x each of {sizes}, one 2-iteration trial per size timed on iteration 2, "
+                      f"oracle/ouro_oracle.cpp on std::thread x {threads}",
+            "per_size": r["per_size"], "verified": r["verified"]}
 
 
 # ------------------------------------------------------------------ GPU ----
@@ -294,7 +320,7 @@ def sweep_floor(per_size, n, max_retries, hot_lat_s, block, p_same):
             "model": "sum over sizes of max(chain floor, OOM-round latency floor) / sum of alloc times"}
 
 
-def job_totals(tot_ms, tot_ok, world, device):
+def job_totals(tot_ms, tot_ok, world, device="cpu"):
     """Whole-job totals for weak scaling: time = MAX over ranks of the device
     time, work = SUM over ranks of successful pairs (independent heaps, no
     collective on the data path; this reduction is bookkeeping only)."""
@@ -324,7 +350,9 @@ def main():
     import paper_2504_18211_b200 as ob
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host-side bookkeeping only (start barrier, max-over-ranks time): every GPU owns
+        # an independent heap and no data crosses GPUs, so no NCCL communicator is made
+        dist.init_process_group("gloo")
     desc, kind, flavor, heap_bytes, n, sizes = CONFIGS[args.config]
     if sizes is None:
         return run_churn(args, world, rank, local, desc, kind, flavor, heap_bytes, n)
@@ -401,7 +429,7 @@ def main():
     err = heap.last_error()
     tot_ms = sum(sum(p["alloc_ms"]) + sum(p["free_ms"]) for p in per.values())
     tot_ok = sum(sum(p["ok"]) for p in per.values())
-    ms_job, ok_job = job_totals(tot_ms, tot_ok, world, "cuda")
+    ms_job, ok_job = job_totals(tot_ms, tot_ok, world)
     value = ok_job / (ms_job / 1e3)
 
     # ---------------- e2e through the public C-ABI with host buffers ----------------
@@ -446,7 +474,7 @@ def main():
             e2e_ok += int(h_res.sum())
 
     # e2e job totals: max over ranks of the e2e time, sum of the successes
-    e2e_ms_job, e2e_ok_job = job_totals(e2e_ms, e2e_ok, world, "cuda")
+    e2e_ms_job, e2e_ok_job = job_totals(e2e_ms, e2e_ok, world)
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -494,20 +522,20 @@ def main():
         except Exception as e:  # reported, not fatal
             cpu = {"error": str(e)}
     line = {
-        "metric": "malloc+free pairs/s (successful), size sweep; % of L2-atomic roofline",
+        "metric": _metric(),
         "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_job / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32/u64 (integer allocator; no floating point)",
         "data": "synthetic",
-        "config": {"workload": desc, "variant": ob.variant_name(hc.variant), "heap_bytes": heap_bytes,
-                   "threads": n, "sizes": sizes, "l2": "flushed (256 MiB write) before every timed kernel",
-                   "timed": "alloc kernel + free kernel per size, CUDA events, default stream",
-                   "per_size": per_size,
-                   "pairs_per_s_16B_1KiB": band_ok / (band_ms / 1e3) if band_ms else None,
-                   "pairs_per_s_sizes_without_oom": full_ok / (full_ms / 1e3) if full_ms else None,
-                   "sizes_without_oom": full,
-                   "verify_mismatched_words": sum(p["verify_bad"] for p in per.values()),
-                   "sticky_error": err[0], "wall_s_timed": wall},
+        "config": dict(config_dict(args.config),
+                       l2="flushed (256 MiB write) before every timed kernel",
+                       timed="alloc kernel + free kernel per size, CUDA events, default stream",
+                       per_size=per_size,
+                       pairs_per_s_16B_1KiB=band_ok / (band_ms / 1e3) if band_ms else None,
+                       pairs_per_s_sizes_without_oom=full_ok / (full_ms / 1e3) if full_ms else None,
+                       sizes_without_oom=full,
+                       verify_mismatched_words=sum(p["verify_bad"] for p in per.values()),
+                       sticky_error=err[0], wall_s_timed=wall, sizes=sizes),
         "roofline": {"bound": "l2_atomic", "kernel": dom,
                      "resource": "same-address RMW chain on the class-queue counters (1 per warp group)",
                      "achieved": achieved / 1e9, "peak": p_same / 1e9, "unit": "Gop/s",
@@ -576,7 +604,7 @@ def run_churn(args, world, rank, local, desc, kind, flavor, heap_bytes, n):
             r0 += CHURN_ROUNDS_PER_STEP
     ok, failed, frees, reused, bad = [int(x) for x in res]
     ops = ok + failed + frees
-    ms_job, ops_job = job_totals(ms, ops, world, "cuda")
+    ms_job, ops_job = job_totals(ms, ops, world)
     a = heap.audit(n, slots)
     st = heap.stats()
     assigned = sum(st.cls[k].chunks for k in range(st.num_classes))

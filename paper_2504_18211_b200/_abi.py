@@ -121,6 +121,16 @@ class ChurnResult(C.Structure):
         "mallocs_ok", "mallocs_failed", "frees", "reused", "check_failures")]
 
 
+_VARIANT_NAMES = {(0, 0): "page", (1, 0): "chunk", (0, 1): "va-page", (1, 1): "va-chunk",
+                  (0, 2): "vl-page", (1, 2): "vl-chunk"}
+
+
+def variant_name_of(kind: int, flavor: int) -> str:
+    """variant_name (config.cpp:44-52) without loading the library (the reference
+    bench arm runs on a host without the CUDA build)."""
+    return _VARIANT_NAMES[(int(kind), int(flavor))]
+
+
 def make_steps(steps):
     """steps: list of (op, lane_mask, args[32]) -> ctypes array of ScriptStep."""
     arr = (ScriptStep * max(1, len(steps)))()
