@@ -348,6 +348,8 @@ def main():
     import torch.distributed as dist
 
     import paper_2504_18211_b200 as ob
+    if args.gpus > 1 and world == 1 and CONFIGS[args.config][5] is not None:
+        return run_threads_driver(args)
     torch.cuda.set_device(local)
     if world > 1:
         # host-side bookkeeping only (start barrier, max-over-ranks time): every GPU owns
@@ -360,7 +362,7 @@ def main():
         sizes = [int(x) for x in args.sizes.split(",")]
     hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
     heap = ob.Heap(hc, local)
-    ob.check(ob.lib().ouro_set_launch_shape(args.block, args.waves), "launch shape")
+    heap.set_launch_shape(args.block, args.waves)
     ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
     res = torch.zeros(4, dtype=torch.int64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -568,6 +570,30 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_threads_driver(args):
+    """--gpus N without torchrun: one process, one host thread and one heap per GPU
+    (ouro_multi_sweep, paper_2504_18211_b200/csrc/ouro_multi.cpp): a host barrier
+    before every step, CUDA events per device, no collective.  value = pairs summed
+    over GPUs / the slowest GPU's summed alloc + free kernel time (weak scaling)."""
+    import paper_2504_18211_b200 as ob
+    desc, kind, flavor, heap_bytes, n, sizes = CONFIGS[args.config]
+    if args.sizes:
+        sizes = [int(x) for x in args.sizes.split(",")]
+    hc = ob.HeapConfig(heap_bytes, allocator_kind=ob.AllocatorKind(kind), queue_flavor=ob.QueueFlavor(flavor))
+    with ClockSampler(0) as clk:
+        r = ob.multi_sweep(hc, list(range(args.gpus)), n, sizes, warmup=args.warmup, steps=args.steps)
+    print(json.dumps({
+        "metric": _metric(), "value": r.pairs_per_s, "unit": "pairs/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r.max_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64 (integer allocator; no floating point)", "data": "synthetic",
+        "config": dict(config_dict(args.config), sizes=sizes,
+                       driver="one process, one host thread + heap per GPU (ouro_multi_sweep), no collective",
+                       per_gpu_ms=[r.dev_ms[d] for d in range(r.ndev)],
+                       per_gpu_pairs=[r.dev_pairs[d] for d in range(r.ndev)], verified=bool(r.verified)),
+        "e2e": None, "gpu_launches": args.gpus * (args.warmup + args.steps) * len(sizes) * 3,
+        "clocks": clk.summary(), "cpu_baseline": None}))
 
 
 def run_churn(args, world, rank, local, desc, kind, flavor, heap_bytes, n):

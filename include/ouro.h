@@ -171,11 +171,13 @@ ouro_status ouro_heap_reset(ouro_heap* heap, void* stream);
 /* Copy the POD device view (struct ouro_heap_view in ouro_device.cuh). */
 ouro_status ouro_heap_get_view(const ouro_heap* heap, void* view_out, size_t view_size);
 size_t ouro_heap_view_size(void);
-/* Launch shape of the alloc/free/churn launchers (process-wide): threads per
+/* Default launch shape of the alloc/free/churn launchers of heaps created later: threads per
  * block (multiple of 32, <= 256); waves: 0 = one thread per request, w >= 1 =
  * persistent grid of w x resident blocks that grid-strides (measured slower,
  * DESIGN.md section 4).  Default 256, 0. */
 ouro_status ouro_set_launch_shape(int block_threads, int waves);
+/* The same for one heap (launch shape is per heap; new heaps take the process default). */
+ouro_status ouro_heap_set_launch_shape(ouro_heap* heap, int block_threads, int waves);
 /* Debug mode: verify queue/bitmap invariants on every device op (CorruptionError
  * on mismatch).  Off by default; affects views fetched afterwards. */
 ouro_status ouro_heap_set_checks(ouro_heap* heap, int on);
@@ -292,6 +294,28 @@ typedef struct ouro_trial_result {
 ouro_status ouro_run_trial(ouro_heap* heap, const ouro_trial_config* cfg, ouro_trial_result* out);
 /* mean_all / mean_subsequent. */
 ouro_status ouro_trial_means(const double* ms, uint32_t n, double* mean_all, double* mean_subsequent);
+
+/* ---------------- multi-device driver (BASELINE configs[4]) ----------------
+ * One host thread per device, each with its own heap (cfg) in its own HBM, a host
+ * barrier before every step; a step runs every size once: alloc kernel of
+ * threads_per_device requests, count, free kernel, each timed kernel after an L2
+ * flush, CUDA events per device.  No collective: pointers never cross devices.
+ * Devices may repeat (several heaps on one device).  Aggregate (weak scaling) =
+ * pairs summed over devices / the slowest device's summed alloc + free time.
+ * Replaces the paper driver's single-device loop for N GPUs. */
+#define OURO_MAX_DEVICES 16
+typedef struct ouro_multi_result {
+    uint32_t ndev;
+    uint32_t verified;            /* 1 iff every device's sticky error word stayed 0 */
+    uint64_t pairs_total;         /* successful malloc+free pairs over devices and timed steps */
+    double max_ms;                /* max over devices of its summed alloc + free kernel time */
+    double pairs_per_s;           /* pairs_total / max_ms */
+    double dev_ms[OURO_MAX_DEVICES];
+    uint64_t dev_pairs[OURO_MAX_DEVICES];
+} ouro_multi_result;
+ouro_status ouro_multi_sweep(const ouro_config* cfg, uint32_t ndev, const int* devices,
+                             uint64_t threads_per_device, const uint32_t* sizes, uint32_t nsizes,
+                             uint32_t warmup, uint32_t steps, ouro_multi_result* out);
 
 /* ---------------- micro-benchmarks for the roofline denominators ---------------- */
 /* mode 0: distinct-address 32-bit atomicAdd (one per 32 B sector, coalesced);

@@ -24,14 +24,14 @@ import os
 from dataclasses import dataclass, field
 
 from . import _abi
-from ._abi import (AuditResult, ChurnResult, Config, Digest, Geometry, ScriptStep, Stats,
+from ._abi import (AuditResult, ChurnResult, Config, Digest, Geometry, MultiResult, ScriptStep, Stats,
                    TrialConfig, TrialResult, make_steps)
 
 __all__ = [
     "HeapConfig", "QueueFlavor", "AllocatorKind", "BackoffPolicy", "Variant", "ALL_VARIANTS",
     "variant_name", "variant_from_name", "Heap", "OuroError", "ConfigError",
     "InvalidHandleError", "DoubleFreeError", "RangeError", "TimeoutError_", "CorruptionError",
-    "lib", "lib_path", "size_class", "backoff_ns",
+    "lib", "lib_path", "size_class", "backoff_ns", "multi_sweep",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -75,6 +75,10 @@ def _declare(L):
         "ouro_heap_view_size": (C.c_size_t, []),
         "ouro_heap_set_checks": (i32, [P, C.c_int]),
         "ouro_set_launch_shape": (i32, [C.c_int, C.c_int]),
+        "ouro_heap_set_launch_shape": (i32, [P, C.c_int, C.c_int]),
+        "ouro_multi_sweep": (i32, [C.POINTER(Config), u32, C.POINTER(C.c_int), u64, C.POINTER(u32), u32, u32, u32,
+                                   C.POINTER(MultiResult)]),
+        "ouro_debug_counters": (i32, [C.POINTER(u64), C.c_int]),
         "ouro_heap_config": (i32, [P, C.POINTER(Config), C.POINTER(Geometry)]),
         "ouro_heap_base": (u64, [P]),
         "ouro_page_region": (i32, [P, u32, C.POINTER(u64), C.POINTER(u64)]),
@@ -354,32 +358,60 @@ class Heap:
         check(st, "page_region")
         return off.value, ln.value
 
+    def set_launch_shape(self, block_threads=256, waves=0):
+        """Launch shape of this heap's alloc/free/churn launchers (ouro_heap_set_launch_shape)."""
+        check(lib().ouro_heap_set_launch_shape(self._h, block_threads, waves), "set_launch_shape")
+
     # ---- driver phases (device buffers: torch tensors or raw pointers) ----
+    def _check_buf(self, x, n, what, dtypes=None, min_elems=None):
+        """Tensors handed to the launchers: on this heap's device, of an accepted
+        dtype, with room for n elements (the kernels index [0, n) unchecked)."""
+        if x is None or isinstance(x, int):
+            return
+        dev = getattr(x, "device", None)
+        if dev is not None and (dev.type != "cuda" or (dev.index if dev.index is not None else 0) != self.device):
+            raise ValueError(f"{what}: tensor on {dev}, heap on cuda:{self.device}")
+        if dtypes is not None and str(x.dtype).replace("torch.", "") not in dtypes:
+            raise ValueError(f"{what}: dtype {x.dtype} not one of {sorted(dtypes)}")
+        if x.numel() < (n if min_elems is None else min_elems):
+            raise ValueError(f"{what}: {x.numel()} elements < {n}")
+
     def launch_alloc(self, n, out_ptrs, size=0, sizes=None, stream=None):
         """sizes: optional device array of per-slot request sizes, int32 or int16/uint16."""
+        self._check_buf(out_ptrs, n, "out_ptrs", {"int64", "uint64"})
+        self._check_buf(sizes, n, "sizes", {"int32", "uint32", "int16", "uint16"})
         if sizes is not None and getattr(sizes, "element_size", lambda: 4)() == 2:
             check(lib().ouro_launch_alloc_u16(self._h, n, _ptr(sizes), _ptr(out_ptrs), _stream(stream)), "alloc")
             return
         check(lib().ouro_launch_alloc(self._h, n, size, _ptr(sizes), _ptr(out_ptrs), _stream(stream)), "alloc")
 
     def launch_free(self, n, ptrs, stream=None):
+        self._check_buf(ptrs, n, "ptrs", {"int64", "uint64"})
         check(lib().ouro_launch_free(self._h, n, _ptr(ptrs), _stream(stream)), "free")
 
     def launch_write(self, n, ptrs, seed, iteration, stream=None):
+        self._check_buf(ptrs, n, "ptrs", {"int64", "uint64"})
         check(lib().ouro_launch_write(self._h, n, _ptr(ptrs), seed, iteration, _stream(stream)), "write")
 
     def launch_verify(self, n, ptrs, seed, iteration, result, stream=None):
+        self._check_buf(ptrs, n, "ptrs", {"int64", "uint64"})
+        self._check_buf(result, 2, "result", {"int64", "uint64"})
         check(lib().ouro_launch_verify(self._h, n, _ptr(ptrs), seed, iteration, _ptr(result),
                                        _stream(stream)), "verify")
 
     def launch_count(self, n, ptrs, count, stream=None):
+        self._check_buf(ptrs, n, "ptrs", {"int64", "uint64"})
+        self._check_buf(count, 1, "count", {"int64", "uint64"})
         check(lib().ouro_launch_count(self._h, n, _ptr(ptrs), _ptr(count), _stream(stream)), "count")
 
     def launch_churn(self, n, round_begin, rounds, seed, slots, result, stream=None):
+        self._check_buf(slots, n, "slots", {"int64", "uint64"})
+        self._check_buf(result, 5, "result", {"int64", "uint64"})
         check(lib().ouro_launch_churn(self._h, n, round_begin, rounds, seed, _ptr(slots), _ptr(result),
                                       _stream(stream)), "churn")
 
     def audit(self, n, ptrs, stream=None) -> AuditResult:
+        self._check_buf(ptrs, n, "ptrs", {"int64", "uint64"})
         r = AuditResult()
         check(lib().ouro_audit(self._h, n, _ptr(ptrs), C.byref(r), _stream(stream)), "audit")
         return r
@@ -405,6 +437,19 @@ class Heap:
         r = TrialResult()
         check(lib().ouro_run_trial(self._h, C.byref(tc), C.byref(r)), "run_trial")
         return r
+
+
+def multi_sweep(cfg: HeapConfig, devices, threads_per_device, sizes, warmup=1, steps=3) -> MultiResult:
+    """ouro_multi_sweep: one host thread and one heap per entry of `devices` (devices may
+    repeat), every step runs the size sweep on all of them behind a host barrier;
+    aggregate pairs/s = pairs over devices / the slowest device's alloc + free time."""
+    devs = (C.c_int * len(devices))(*devices)
+    sz = (C.c_uint32 * len(sizes))(*sizes)
+    r = MultiResult()
+    c = cfg.to_c()
+    check(lib().ouro_multi_sweep(C.byref(c), len(devices), devs, threads_per_device, sz, len(sizes), warmup, steps,
+                                 C.byref(r)), "multi_sweep")
+    return r
 
 
 def atomic_peak(device: int, mode: int) -> float:

@@ -121,6 +121,15 @@ class ChurnResult(C.Structure):
         "mallocs_ok", "mallocs_failed", "frees", "reused", "check_failures")]
 
 
+MAX_DEVICES = 16
+
+
+class MultiResult(C.Structure):
+    _fields_ = [("ndev", C.c_uint32), ("verified", C.c_uint32), ("pairs_total", C.c_uint64),
+                ("max_ms", C.c_double), ("pairs_per_s", C.c_double),
+                ("dev_ms", C.c_double * MAX_DEVICES), ("dev_pairs", C.c_uint64 * MAX_DEVICES)]
+
+
 _VARIANT_NAMES = {(0, 0): "page", (1, 0): "chunk", (0, 1): "va-page", (1, 1): "va-chunk",
                   (0, 2): "vl-page", (1, 2): "vl-chunk"}
 

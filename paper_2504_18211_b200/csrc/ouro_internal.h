@@ -42,4 +42,7 @@ struct ouro_heap {
     int64_t floor_F = 0;
     ouro_heap_view view{};
     uint32_t nq = 0;
+    // launch shape of this heap's alloc/free/churn launchers (ouro_heap_set_launch_shape)
+    int op_block = 256;
+    int op_waves = 0;
 };

@@ -13,7 +13,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -42,24 +46,71 @@ namespace {
 constexpr int kBlock = 256;
 constexpr size_t kSmHintBytes = 256 * 32 * 8;
 // Launch shape of the malloc/free/churn drivers (one request per thread, requests
-// independent).  g_op_waves = 0: one thread per request (grid = n / block);
-// g_op_waves = w >= 1: persistent grid of w x (resident CTAs per SM) x SMs that
-// grid-strides over the requests.  Persistent CTAs keep their shared-memory poll
-// state (ouro_device.cuh "poll combining") across requests, so an OOM storm pays
-// one count RMW+undo per CTA instead of per warp.
-int g_op_block = 256;
-int g_op_waves = 0;
+// independent), per heap; new heaps start from the process default
+// (ouro_set_launch_shape).  op_waves = 0: one thread per request (grid = n /
+// block); op_waves = w >= 1: persistent grid of w x (resident CTAs per SM) x SMs
+// that grid-strides over the requests (measured slower).
+std::atomic<int> g_def_block{256};
+std::atomic<int> g_def_waves{0};
 template <class Kern>
-unsigned op_grid(Kern kern, u64 n) {
-    const u64 need = std::max<u64>(1, (n + g_op_block - 1) / g_op_block);
-    if (g_op_waves <= 0) return (unsigned)need;
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, g_op_block, 0);
-    const u64 cap = (u64)std::max(1, per_sm) * (u64)std::max(1, sms) * (u64)g_op_waves;
+unsigned op_grid(const ouro_heap* H, Kern kern, u64 n) {
+    const u64 need = std::max<u64>(1, (n + H->op_block - 1) / H->op_block);
+    if (H->op_waves <= 0) return (unsigned)need;
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, H->op_block, 0);
+    const u64 cap = (u64)std::max(1, per_sm) * (u64)std::max(1, sms) * (u64)H->op_waves;
     return (unsigned)std::min(need, cap);
 }
+
+// Every host entry point that touches a heap runs on the heap's device and
+// restores the caller's current device on return (several heaps on several
+// devices may be driven from one host thread, or one heap per host thread).
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) { prev = -1; ok = false; return; }
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+#define OURO_BIND(H)                                   \
+    DeviceGuard dev_guard_((H)->device);               \
+    if (!dev_guard_.ok) return OURO_ERR_CUDA
+
+// Scoped device buffer / event / stream: released on every return path.
+struct DevBuf {
+    void* p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { if (p) cudaFree(p); }
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, std::max<size_t>(bytes, 16)); }
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+struct Events {
+    std::vector<cudaEvent_t> ev;
+    ~Events() { for (auto e : ev) cudaEventDestroy(e); }
+    cudaError_t create(size_t n) {
+        for (size_t i = 0; i < n; ++i) {
+            cudaEvent_t e;
+            const cudaError_t r = cudaEventCreate(&e);
+            if (r != cudaSuccess) return r;
+            ev.push_back(e);
+        }
+        return cudaSuccess;
+    }
+};
+struct Stream {
+    cudaStream_t s = nullptr;
+    ~Stream() { if (s) cudaStreamDestroy(s); }
+};
 
 __host__ __device__ inline u64 mix64h(u64 x) {
     x += 0x9E3779B97F4A7C15ull;
@@ -517,19 +568,19 @@ __global__ void k_atom_same_lane(u64* a, u32 iters) {
 
 template <int K, int F>
 void launch_alloc(ouro_heap* H, u64 n, u64 uni, const u32* sizes, void** out, cudaStream_t st) {
-    k_alloc<K, F><<<op_grid(k_alloc<K, F>, n), g_op_block, 0, st>>>(H->view, n, uni, sizes, out);
+    k_alloc<K, F><<<op_grid(H, k_alloc<K, F>, n), H->op_block, 0, st>>>(H->view, n, uni, sizes, out);
 }
 template <int K, int F>
 void launch_alloc16(ouro_heap* H, u64 n, const uint16_t* sizes, void** out, cudaStream_t st) {
-    k_alloc<K, F, uint16_t><<<op_grid(k_alloc<K, F, uint16_t>, n), g_op_block, 0, st>>>(H->view, n, 0, sizes, out);
+    k_alloc<K, F, uint16_t><<<op_grid(H, k_alloc<K, F, uint16_t>, n), H->op_block, 0, st>>>(H->view, n, 0, sizes, out);
 }
 template <int K, int F>
 void launch_free(ouro_heap* H, u64 n, void* const* p, cudaStream_t st) {
-    k_free<K, F><<<op_grid(k_free<K, F>, n), g_op_block, 0, st>>>(H->view, n, p);
+    k_free<K, F><<<op_grid(H, k_free<K, F>, n), H->op_block, 0, st>>>(H->view, n, p);
 }
 template <int K, int F>
 void launch_churn(ouro_heap* H, u64 n, u32 r, u64 seed, void** slots, u64* res, cudaStream_t st) {
-    k_churn<K, F><<<op_grid(k_churn<K, F>, n), g_op_block, 0, st>>>(H->view, n, r, seed, slots, H->d_touched, res);
+    k_churn<K, F><<<op_grid(H, k_churn<K, F>, n), H->op_block, 0, st>>>(H->view, n, r, seed, slots, H->d_touched, res);
 }
 template <int K, int F>
 void launch_script(ouro_heap* H, const ouro_script_step* s, u32 n, u64* o, int* st) {
@@ -771,11 +822,13 @@ ouro_status compute_digest(ouro_heap* H, ouro_digest* out, DigestDev* hd_out, st
                            cudaStream_t st) {
     const Geometry& g = H->g;
     const u32 N = g.N, K = g.K;
-    DigestDev* d = nullptr;
-    u32 *where = nullptr, *entries = nullptr;
-    CK(cudaMalloc(&d, sizeof(DigestDev)));
-    CK(cudaMalloc(&where, (size_t)N * 4));
-    CK(cudaMalloc(&entries, (size_t)N * 4));
+    DevBuf d_buf, where_buf, entries_buf;
+    CK(d_buf.alloc(sizeof(DigestDev)));
+    CK(where_buf.alloc((size_t)N * 4));
+    CK(entries_buf.alloc((size_t)N * 4));
+    DigestDev* d = d_buf.as<DigestDev>();
+    u32* where = where_buf.as<u32>();
+    u32* entries = entries_buf.as<u32>();
     CK(cudaMemsetAsync(d, 0, sizeof(DigestDev), st));
     CK(cudaMemsetAsync(where, 0, (size_t)N * 4, st));
     CK(cudaMemsetAsync(entries, 0, (size_t)N * 4, st));
@@ -844,16 +897,17 @@ ouro_status compute_digest(ouro_heap* H, ouro_digest* out, DigestDev* hd_out, st
         std::vector<u32> tab;
         u64 first;
         if (segtab_of(q, tab, first) != OURO_OK) return OURO_ERR_CUDA;
+        DevBuf dtab_buf;
         u32* dtab = nullptr;
         if (!tab.empty()) {
-            CK(cudaMalloc(&dtab, tab.size() * 4));
+            CK(dtab_buf.alloc(tab.size() * 4));
+            dtab = dtab_buf.as<u32>();
             CK(cudaMemcpy(dtab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
         }
         k_digest_queue<<<(unsigned)std::min<u64>((n + kBlock - 1) / kBlock, 148 * 32), kBlock, 0, st>>>(
             H->view, H->d_q + qi, dtab, first, mode, k, d, where, entries);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
-        if (dtab) cudaFree(dtab);
         return OURO_OK;
     };
     if (H->cfg.allocator_kind == OURO_KIND_CHUNK) {
@@ -881,9 +935,6 @@ ouro_status compute_digest(ouro_heap* H, ouro_digest* out, DigestDev* hd_out, st
     u32 sticky[2];
     CK(cudaMemcpyAsync(sticky, H->d_sticky, 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    cudaFree(d);
-    cudaFree(where);
-    cudaFree(entries);
     bool ok = hd.bad == 0 && !host_bad;
     const bool dbg = std::getenv("OURO_DIGEST_DEBUG") != nullptr;
     if (dbg && !ok) std::fprintf(stderr, "digest: dev bad %u host_bad %d\n", (unsigned)hd.bad, (int)host_bad);
@@ -930,12 +981,15 @@ ouro_status ouro_heap_create(const ouro_config* cfg, int device, ouro_heap** out
     ouro_host::Geometry g;
     if (ouro_host::geometry(cfg, &g) != OURO_OK) return OURO_ERR_CONFIG;
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= device) return OURO_ERR_CUDA;
-    CK(cudaSetDevice(device));
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || ndev <= device) return OURO_ERR_CUDA;
+    DeviceGuard dev_guard_(device);  // the caller's current device is restored on return
+    if (!dev_guard_.ok) return OURO_ERR_CUDA;
     auto* H = new ouro_heap();
     H->cfg = *cfg;
     H->g = g;
     H->device = device;
+    H->op_block = g_def_block.load();
+    H->op_waves = g_def_waves.load();
     auto fail = [&](ouro_status s) { ouro_heap_destroy(H); return s; };
     H->d_heap = static_cast<uint8_t*>(dalloc(H, g.heap));
     H->d_meta = static_cast<u64*>(dalloc(H, (size_t)g.N * 8));
@@ -958,7 +1012,7 @@ ouro_status ouro_heap_create(const ouro_config* cfg, int device, ouro_heap** out
 
 ouro_status ouro_heap_destroy(ouro_heap* H) {
     if (!H) return OURO_ERR_USAGE;
-    cudaSetDevice(H->device);
+    DeviceGuard dev_guard_(H->device);
     for (void* p : H->owned) cudaFree(p);
     if (H->d_touched) cudaFree(H->d_touched);
     delete H;
@@ -967,7 +1021,7 @@ ouro_status ouro_heap_destroy(ouro_heap* H) {
 
 ouro_status ouro_heap_reset(ouro_heap* H, void* stream) {
     if (!H) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     CK(cudaStreamSynchronize(S(stream)));
     return fill(H, S(stream));
 }
@@ -976,8 +1030,15 @@ size_t ouro_heap_view_size(void) { return sizeof(ouro_heap_view); }
 
 ouro_status ouro_set_launch_shape(int block_threads, int waves) {
     if (block_threads < 32 || block_threads > kBlock || block_threads % 32 || waves < 0) return OURO_ERR_USAGE;
-    g_op_block = block_threads;
-    g_op_waves = waves;
+    g_def_block = block_threads;
+    g_def_waves = waves;
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_set_launch_shape(ouro_heap* H, int block_threads, int waves) {
+    if (!H || block_threads < 32 || block_threads > kBlock || block_threads % 32 || waves < 0) return OURO_ERR_USAGE;
+    H->op_block = block_threads;
+    H->op_waves = waves;
     return OURO_OK;
 }
 
@@ -1008,6 +1069,7 @@ ouro_status ouro_page_region(ouro_heap* H, uint32_t h, uint64_t* offset, uint64_
     const u64 c = (u64)h >> g.page_bits;
     const u32 p = h & ((1u << g.page_bits) - 1u);
     if (c >= g.N) return OURO_ERR_RANGE;
+    OURO_BIND(H);
     u64 m;
     CK(cudaMemcpy(&m, H->d_meta + c, 8, cudaMemcpyDeviceToHost));
     const u32 st = (u32)(m >> 32) & 0xFF;
@@ -1021,6 +1083,7 @@ ouro_status ouro_page_region(ouro_heap* H, uint32_t h, uint64_t* offset, uint64_
 
 ouro_status ouro_heap_last_error(ouro_heap* H, uint32_t* first, uint32_t* mask, int clear) {
     if (!H) return OURO_ERR_USAGE;
+    OURO_BIND(H);
     u32 s[2];
     CK(cudaMemcpy(s, H->d_sticky, 8, cudaMemcpyDeviceToHost));
     if (first) *first = s[0];
@@ -1031,14 +1094,14 @@ ouro_status ouro_heap_last_error(ouro_heap* H, uint32_t* first, uint32_t* mask, 
 
 ouro_status ouro_heap_digest(ouro_heap* H, ouro_digest* out, void* stream) {
     if (!H || !out) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     CK(cudaStreamSynchronize(S(stream)));
     return compute_digest(H, out, nullptr, nullptr, S(stream));
 }
 
 ouro_status ouro_heap_queue_links(ouro_heap* H, uint32_t qi, uint64_t out[4]) {
     if (!H || !out || qi >= H->nq) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     CK(cudaDeviceSynchronize());
     const ouro_queue_dev* q = H->d_q + qi;
     CK(cudaMemcpy(&out[0], &q->count, 8, cudaMemcpyDeviceToHost));
@@ -1050,7 +1113,7 @@ ouro_status ouro_heap_queue_links(ouro_heap* H, uint32_t qi, uint64_t out[4]) {
 
 ouro_status ouro_heap_vl_ring(ouro_heap* H, uint32_t qi, uint64_t out[OURO_VL_RECENT]) {
     if (!H || !out || qi >= H->nq) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out, &(H->d_q + qi)->vl_deq[0], 8 * OURO_VL_RECENT, cudaMemcpyDeviceToHost));
     return OURO_OK;
@@ -1058,7 +1121,7 @@ ouro_status ouro_heap_vl_ring(ouro_heap* H, uint32_t qi, uint64_t out[OURO_VL_RE
 
 ouro_status ouro_heap_stats(ouro_heap* H, ouro_stats* out, void* stream) {
     if (!H || !out) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     CK(cudaStreamSynchronize(S(stream)));
     ouro_digest dg;
     DigestDev hd;
@@ -1106,6 +1169,7 @@ ouro_status ouro_launch_alloc(ouro_heap* H, uint64_t n, uint64_t uniform_bytes, 
                               void* stream) {
     if (!H || !d_out) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     OURO_VSWITCH(H, launch_alloc, H, n, uniform_bytes, d_sizes, d_out, S(stream));
     CK(cudaGetLastError());
     return OURO_OK;
@@ -1114,6 +1178,7 @@ ouro_status ouro_launch_alloc(ouro_heap* H, uint64_t n, uint64_t uniform_bytes, 
 ouro_status ouro_launch_alloc_u16(ouro_heap* H, uint64_t n, const uint16_t* d_sizes, void** d_out, void* stream) {
     if (!H || !d_out || !d_sizes) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     OURO_VSWITCH(H, launch_alloc16, H, n, d_sizes, d_out, S(stream));
     CK(cudaGetLastError());
     return OURO_OK;
@@ -1122,6 +1187,7 @@ ouro_status ouro_launch_alloc_u16(ouro_heap* H, uint64_t n, const uint16_t* d_si
 ouro_status ouro_launch_free(ouro_heap* H, uint64_t n, void* const* d_ptrs, void* stream) {
     if (!H || !d_ptrs) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     OURO_VSWITCH(H, launch_free, H, n, d_ptrs, S(stream));
     CK(cudaGetLastError());
     return OURO_OK;
@@ -1130,6 +1196,7 @@ ouro_status ouro_launch_free(ouro_heap* H, uint64_t n, void* const* d_ptrs, void
 ouro_status ouro_launch_write(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t seed, uint32_t it, void* stream) {
     if (!H || !d_ptrs) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     k_pattern<false><<<pattern_grid(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it, nullptr);
     CK(cudaGetLastError());
     return OURO_OK;
@@ -1139,6 +1206,7 @@ ouro_status ouro_launch_verify(ouro_heap* H, uint64_t n, void* const* d_ptrs, ui
                                uint64_t* d_result, void* stream) {
     if (!H || !d_ptrs || !d_result) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     k_pattern<true><<<pattern_grid(n), kBlock, 0, S(stream)>>>(H->view, n, d_ptrs, seed, it,
                                                               reinterpret_cast<u64*>(d_result));
     CK(cudaGetLastError());
@@ -1148,6 +1216,7 @@ ouro_status ouro_launch_verify(ouro_heap* H, uint64_t n, void* const* d_ptrs, ui
 ouro_status ouro_launch_count(ouro_heap* H, uint64_t n, void* const* d_ptrs, uint64_t* d_count, void* stream) {
     if (!H || !d_ptrs || !d_count) return OURO_ERR_USAGE;
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     k_count<<<grid_for(n), kBlock, 0, S(stream)>>>(n, d_ptrs, reinterpret_cast<u64*>(d_count));
     CK(cudaGetLastError());
     return OURO_OK;
@@ -1157,15 +1226,18 @@ ouro_status ouro_audit(ouro_heap* H, uint64_t n, void* const* d_ptrs, ouro_audit
     if (!H || !d_ptrs || !out) return OURO_ERR_USAGE;
     std::memset(out, 0, sizeof(*out));
     if (n == 0) return OURO_OK;
+    OURO_BIND(H);
     cudaStream_t st = S(stream);
-    u64 *offs, *lens, *offs2, *lens2, *res;
-    unsigned long long* idx;
-    CK(cudaMalloc(&offs, n * 8));
-    CK(cudaMalloc(&lens, n * 8));
-    CK(cudaMalloc(&offs2, n * 8));
-    CK(cudaMalloc(&lens2, n * 8));
-    CK(cudaMalloc(&res, 8 * 8));
-    CK(cudaMalloc(&idx, 8));
+    DevBuf offs_b, lens_b, offs2_b, lens2_b, res_b, idx_b;
+    CK(offs_b.alloc(n * 8));
+    CK(lens_b.alloc(n * 8));
+    CK(offs2_b.alloc(n * 8));
+    CK(lens2_b.alloc(n * 8));
+    CK(res_b.alloc(8 * 8));
+    CK(idx_b.alloc(8));
+    u64 *offs = offs_b.as<u64>(), *lens = lens_b.as<u64>(), *offs2 = offs2_b.as<u64>(), *lens2 = lens2_b.as<u64>();
+    u64* res = res_b.as<u64>();
+    unsigned long long* idx = idx_b.as<unsigned long long>();
     CK(cudaMemsetAsync(res, 0, 64, st));
     CK(cudaMemsetAsync(idx, 0, 8, st));
     k_audit_collect<<<grid_for(n), kBlock, 0, st>>>(H->view, n, d_ptrs, offs, lens, res, idx);
@@ -1175,14 +1247,13 @@ ouro_status ouro_audit(ouro_heap* H, uint64_t n, void* const* d_ptrs, ouro_audit
     CK(cudaStreamSynchronize(st));
     if (m > 1) {
         size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st);
-        void* tmp;
-        CK(cudaMalloc(&tmp, tb));
-        cub::DeviceRadixSort::SortPairs(tmp, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st);
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st));
+        DevBuf tmp;
+        CK(tmp.alloc(tb));
+        CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, offs, offs2, lens, lens2, (int)m, 0, 64, st));
         k_audit_neighbours<<<grid_for(m), kBlock, 0, st>>>(m, offs2, lens2, res);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
-        cudaFree(tmp);
     }
     u64 r[8];
     CK(cudaMemcpyAsync(r, res, 64, cudaMemcpyDeviceToHost, st));
@@ -1193,13 +1264,13 @@ ouro_status ouro_audit(ouro_heap* H, uint64_t n, void* const* d_ptrs, ouro_audit
     out->overlaps = r[3];
     out->not_marked = r[4];
     out->bytes = r[5];
-    cudaFree(offs); cudaFree(lens); cudaFree(offs2); cudaFree(lens2); cudaFree(res); cudaFree(idx);
     return OURO_OK;
 }
 
 ouro_status ouro_launch_churn(ouro_heap* H, uint64_t n, uint32_t round_begin, uint32_t rounds, uint64_t seed,
                               void** d_slots, uint64_t* d_result, void* stream) {
     if (!H || !d_slots || !d_result) return OURO_ERR_USAGE;
+    OURO_BIND(H);
     if (!H->d_touched) {
         const size_t b = H->g.heap / H->g.minp / 8 + 8;
         CK(cudaMalloc(&H->d_touched, b));
@@ -1215,63 +1286,73 @@ ouro_status ouro_launch_churn(ouro_heap* H, uint64_t n, uint32_t round_begin, ui
 ouro_status ouro_run_script(ouro_heap* H, const ouro_script_step* steps, uint32_t nsteps, uint64_t* out_offset,
                             int32_t* out_status) {
     if (!H || !steps || !out_offset || !out_status) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
-    ouro_script_step* ds;
-    u64* doff;
-    int* dst;
-    CK(cudaMalloc(&ds, (size_t)nsteps * sizeof(ouro_script_step) + 1));
-    CK(cudaMalloc(&doff, (size_t)nsteps * 32 * 8 + 8));
-    CK(cudaMalloc(&dst, (size_t)nsteps * 32 * 4 + 4));
+    OURO_BIND(H);
+    DevBuf ds_b, doff_b, dst_b;
+    CK(ds_b.alloc((size_t)nsteps * sizeof(ouro_script_step) + 1));
+    CK(doff_b.alloc((size_t)nsteps * 32 * 8 + 8));
+    CK(dst_b.alloc((size_t)nsteps * 32 * 4 + 4));
+    ouro_script_step* ds = ds_b.as<ouro_script_step>();
+    u64* doff = doff_b.as<u64>();
+    int* dst = dst_b.as<int>();
     CK(cudaMemcpy(ds, steps, (size_t)nsteps * sizeof(ouro_script_step), cudaMemcpyHostToDevice));
     OURO_VSWITCH(H, launch_script, H, ds, nsteps, doff, dst);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     CK(cudaMemcpy(out_offset, doff, (size_t)nsteps * 32 * 8, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(out_status, dst, (size_t)nsteps * 32 * 4, cudaMemcpyDeviceToHost));
-    cudaFree(ds); cudaFree(doff); cudaFree(dst);
     return OURO_OK;
 }
 
-// run_trial: host buffers in, host results out.
+// run_trial: host buffers in, host results out.  Every
+// launcher status is checked; buffers, events and the stream are released on
+// every return path.
 ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial_result* out) {
     if (!H || !tc || !out) return OURO_ERR_USAGE;
     if (tc->iterations < 2 || tc->iterations > 64 || tc->num_allocations == 0) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(H->device));
+    OURO_BIND(H);
     std::memset(out, 0, sizeof(*out));
     const u64 n = tc->num_allocations;
-    cudaStream_t st;
-    CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    void** ptrs;
-    u32* dsz = nullptr;
-    u64* dres;
-    CK(cudaMalloc(&ptrs, n * sizeof(void*)));
-    if (tc->sizes) CK(cudaMalloc(&dsz, n * 4));
-    CK(cudaMalloc(&dres, 4 * 8));
-    cudaEvent_t ev[6];
-    for (auto& e : ev) CK(cudaEventCreate(&e));
+    Stream stream;
+    CK(cudaStreamCreateWithFlags(&stream.s, cudaStreamNonBlocking));
+    cudaStream_t st = stream.s;
+    DevBuf ptrs_b, dsz_b, dres_b;
+    CK(ptrs_b.alloc(n * sizeof(void*)));
+    if (tc->sizes) CK(dsz_b.alloc(n * 4));
+    CK(dres_b.alloc(4 * 8));
+    void** ptrs = ptrs_b.as<void*>();
+    u32* dsz = tc->sizes ? dsz_b.as<u32>() : nullptr;
+    u64* dres = dres_b.as<u64>();
+    Events evs;
+    CK(evs.create(5));
+    cudaEvent_t* ev = evs.ev.data();
     bool verified = true;
+#define OURO_TRY(x)                                  \
+    do {                                             \
+        const ouro_status s_ = (x);                  \
+        if (s_ != OURO_OK) return s_;                \
+    } while (0)
     for (u32 it = 0; it < tc->iterations; ++it) {
         const u64 init[4] = {0, ~0ull, 0, 0};
         CK(cudaMemcpyAsync(dres, init, 32, cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(ev[0], st));
         if (tc->sizes) CK(cudaMemcpyAsync(dsz, tc->sizes, n * 4, cudaMemcpyHostToDevice, st));
-        if (ouro_launch_alloc(H, n, tc->allocation_bytes, dsz, ptrs, st) != OURO_OK) return OURO_ERR_CUDA;
+        OURO_TRY(ouro_launch_alloc(H, n, tc->allocation_bytes, dsz, ptrs, st));
         CK(cudaEventRecord(ev[1], st));
-        ouro_launch_write(H, n, ptrs, tc->seed, it, st);
+        OURO_TRY(ouro_launch_write(H, n, ptrs, tc->seed, it, st));
         CK(cudaEventRecord(ev[2], st));
-        ouro_launch_verify(H, n, ptrs, tc->seed, it, reinterpret_cast<uint64_t*>(dres), st);
-        ouro_launch_count(H, n, ptrs, reinterpret_cast<uint64_t*>(dres + 2), st);
+        OURO_TRY(ouro_launch_verify(H, n, ptrs, tc->seed, it, reinterpret_cast<uint64_t*>(dres), st));
+        OURO_TRY(ouro_launch_count(H, n, ptrs, reinterpret_cast<uint64_t*>(dres + 2), st));
         CK(cudaEventRecord(ev[3], st));
-        ouro_launch_free(H, n, ptrs, st);
+        OURO_TRY(ouro_launch_free(H, n, ptrs, st));
         CK(cudaEventRecord(ev[4], st));
         u64 r[4];
         CK(cudaMemcpyAsync(r, dres, 32, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         float a, w, vv, f;
-        cudaEventElapsedTime(&a, ev[0], ev[1]);
-        cudaEventElapsedTime(&w, ev[1], ev[2]);
-        cudaEventElapsedTime(&vv, ev[2], ev[3]);
-        cudaEventElapsedTime(&f, ev[3], ev[4]);
+        CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        CK(cudaEventElapsedTime(&w, ev[1], ev[2]));
+        CK(cudaEventElapsedTime(&vv, ev[2], ev[3]));
+        CK(cudaEventElapsedTime(&f, ev[3], ev[4]));
         out->alloc_ms[it] = a;
         out->write_ms[it] = w;
         out->verify_ms[it] = vv;
@@ -1280,6 +1361,7 @@ ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial
         out->failed_allocs += n - r[2];
         if (r[0] != 0) verified = false;
     }
+#undef OURO_TRY
     out->iterations = tc->iterations;
     out->verified = verified ? 1 : 0;
     ouro_trial_means(out->alloc_ms, tc->iterations, &out->mean_all_ms, &out->mean_subsequent_ms);
@@ -1287,26 +1369,23 @@ ouro_status ouro_run_trial(ouro_heap* H, const ouro_trial_config* tc, ouro_trial
     ouro_trial_means(out->free_ms, tc->iterations, &fa, &out->mean_subsequent_free_ms);
     out->h2d_bytes = tc->sizes ? n * 4 : 0;
     out->d2h_bytes = 32;
-    for (auto& e : ev) cudaEventDestroy(e);
-    cudaFree(ptrs);
-    if (dsz) cudaFree(dsz);
-    cudaFree(dres);
-    cudaStreamDestroy(st);
     return OURO_OK;
 }
 
 ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     if (!ops_per_s) return OURO_ERR_USAGE;
-    CK(cudaSetDevice(device));
+    DeviceGuard dev_guard_(device);
+    if (!dev_guard_.ok) return OURO_ERR_CUDA;
     const u64 words = 1ull << 22;  // 32 MiB of u64 / 16 MiB of u32 counters: L2-resident (atomics resolve in L2)
-    void* buf;
-    CK(cudaMalloc(&buf, words * 8));
+    DevBuf buf_b;
+    CK(buf_b.alloc(words * 8));
+    void* buf = buf_b.p;
     CK(cudaMemset(buf, 0, words * 8));
     const unsigned blocks = 148 * 8, threads = 256;
     const u32 iters = mode >= 2 ? 64 : 64;
-    cudaEvent_t a, b;
-    CK(cudaEventCreate(&a));
-    CK(cudaEventCreate(&b));
+    Events evs;
+    CK(evs.create(2));
+    cudaEvent_t a = evs.ev[0], b = evs.ev[1];
     auto run = [&]() {
         switch (mode) {
         case 0: k_atom_distinct32<<<blocks, threads>>>((u32*)buf, words * 2, iters); break;
@@ -1334,9 +1413,6 @@ ouro_status ouro_atomic_peak(int device, int mode, double* ops_per_s) {
     if (mode == 3) ops = (double)blocks * threads * (iters / 16);
     if (mode == 4) ops = 2048.0;  // loads of ONE poller (all 888 run concurrently): 1 / hot-word latency
     *ops_per_s = ops / (best * 1e-3);
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    cudaFree(buf);
     return OURO_OK;
 }
 
