@@ -181,6 +181,13 @@ ouro_status ouro_heap_set_launch_shape(ouro_heap* heap, int block_threads, int w
 /* Debug mode: verify queue/bitmap invariants on every device op (CorruptionError
  * on mismatch).  Off by default; affects views fetched afterwards. */
 ouro_status ouro_heap_set_checks(ouro_heap* heap, int on);
+/* Bounded waits (TimeoutError, errors.hpp:35-39): iterations a device wait may
+ * spin before raising OURO_ERR_TIMEOUT in the sticky word and failing the
+ * operation instead of hanging the GPU.  Default 2^22 (~seconds). */
+ouro_status ouro_heap_set_spin_limit(ouro_heap* heap, uint64_t limit);
+/* Test-only fault injection: add delta to queue qi's occupancy count (e.g. a
+ * count that promises entries no slot holds, so a dequeue must time out). */
+ouro_status ouro_heap_debug_add_count(ouro_heap* heap, uint32_t qi, int64_t delta);
 ouro_status ouro_heap_config(const ouro_heap* heap, ouro_config* cfg, ouro_geometry* geo);
 uint64_t ouro_heap_base(const ouro_heap* heap); /* device address of heap byte 0 */
 /* page_region against live device state; InvalidHandle if the

@@ -893,13 +893,13 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
     const u32 c = seg_acquire_zero(v, Q, mask, lane, who);
     if (c == NONE) return false;
     u32 back = NONE, fwd = 0, ok = 1;
+    u64* slot = &Q->vl_recent[(s) & Q->vl_rmask];
     if (lane == who) {
         st_rlx(chunk_words(v, c), NONE_LINK);
         // retire counter 0, in-link flag set only for segment 0 (no predecessor); the
         // chunk may not have been zeroed
         st_rlx(reinterpret_cast<u64*>(vl_counter(v, c)), s == 0 ? (1ull << 32) : 0ull);
         __threadfence();  // the zeroed chunk and its header before the publication
-        u64* slot = &Q->vl_recent[(s) & Q->vl_rmask];
         Spin sp;
         for (;;) {  // the slot's occupant must be fully linked (or retired) before we take it
             const u64 r = ld_rlx(slot);
@@ -908,6 +908,15 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
             if (ld_rlx(chunk_words(v, lchk(r))) != NONE_LINK && ld_rlx32(vl_inflag(v, lchk(r))) != 0) break;
             if (!sp.step(v)) { raise_err(v, OURO_ERR_TIMEOUT); ok = 0; break; }
         }
+    }
+    ok = __shfl_sync(mask, ok, who);
+    if (!ok) {
+        // timed out waiting for the occupant to be linked: do not overwrite it (its
+        // link could be lost and the head stall) -- give the chunk back unpublished
+        arr_enqueue(v, v.q + Q->seg_src, mask, lane, 1u << who, c, true);
+        return false;
+    }
+    if (lane == who) {
         const u64 me = mklink(s, c);
         if (s == 0) st_rlx(&Q->vl_head, me);
         st_rlx(slot, me);  // publish: wakes the enqueuers of s
@@ -924,10 +933,9 @@ __device__ __forceinline__ bool vl_create(const ouro_heap_view& v, ouro_queue_de
     }
     back = __shfl_sync(mask, back, who);
     fwd = __shfl_sync(mask, fwd, who);
-    ok = __shfl_sync(mask, ok, who);
     if (back != NONE) vl_add(v, Q, mask, lane, lane == who, back, 1u);  // link event of s-1
     if (fwd) vl_add(v, Q, mask, lane, lane == who, c, 1u);              // link event of s
-    return ok != 0;
+    return true;
 }
 
 // ------------------------------------------------- flavour-generic queue ----

@@ -74,6 +74,8 @@ def _declare(L):
         "ouro_heap_get_view": (i32, [P, P, C.c_size_t]),
         "ouro_heap_view_size": (C.c_size_t, []),
         "ouro_heap_set_checks": (i32, [P, C.c_int]),
+        "ouro_heap_set_spin_limit": (i32, [P, u64]),
+        "ouro_heap_debug_add_count": (i32, [P, u32, C.c_int64]),
         "ouro_set_launch_shape": (i32, [C.c_int, C.c_int]),
         "ouro_heap_set_launch_shape": (i32, [P, C.c_int, C.c_int]),
         "ouro_multi_sweep": (i32, [C.POINTER(Config), u32, C.POINTER(C.c_int), u64, C.POINTER(u32), u32, u32, u32,
@@ -315,6 +317,14 @@ class Heap:
     def set_checks(self, on: bool = True):
         """Debug mode: verify queue/bitmap invariants on every device op."""
         check(lib().ouro_heap_set_checks(self._h, int(on)), "set_checks")
+
+    def set_spin_limit(self, limit: int):
+        """Bounded device waits: spins before TimeoutError (errors.hpp:35-39)."""
+        check(lib().ouro_heap_set_spin_limit(self._h, limit), "set_spin_limit")
+
+    def debug_add_count(self, qi: int, delta: int):
+        """Test-only fault injection into queue qi's occupancy count."""
+        check(lib().ouro_heap_debug_add_count(self._h, qi, delta), "debug_add_count")
 
     def queue_links(self, qi: int):
         """Debug: (count, head ticket, vl_head, vl_tail) of queue qi."""

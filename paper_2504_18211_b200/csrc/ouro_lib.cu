@@ -1048,6 +1048,23 @@ ouro_status ouro_heap_set_checks(ouro_heap* H, int on) {
     return OURO_OK;
 }
 
+ouro_status ouro_heap_set_spin_limit(ouro_heap* H, uint64_t limit) {
+    if (!H || limit == 0) return OURO_ERR_USAGE;
+    H->view.spin_limit = limit;
+    return OURO_OK;
+}
+
+ouro_status ouro_heap_debug_add_count(ouro_heap* H, uint32_t qi, int64_t delta) {
+    if (!H || qi >= H->nq) return OURO_ERR_USAGE;
+    OURO_BIND(H);
+    CK(cudaDeviceSynchronize());
+    int64_t c;
+    CK(cudaMemcpy(&c, &(H->d_q + qi)->count, 8, cudaMemcpyDeviceToHost));
+    c += delta;
+    CK(cudaMemcpy(&(H->d_q + qi)->count, &c, 8, cudaMemcpyHostToDevice));
+    return OURO_OK;
+}
+
 ouro_status ouro_heap_get_view(const ouro_heap* H, void* out, size_t size) {
     if (!H || !out || size < sizeof(ouro_heap_view)) return OURO_ERR_USAGE;
     std::memcpy(out, &H->view, sizeof(ouro_heap_view));
