@@ -76,6 +76,7 @@ enum {
     OURO_CTR_TIMEOUT = 4,
     OURO_CTR_CORRUPTION = 5,
     OURO_CTR_POOL_DEQ = 6,
+    OURO_CTR_CLAIM_RETRY = 7,   /* chunk-bitmap picks lost to a concurrent holder (retried) */
     OURO_CTR_N = 8
 };
 /* ctr[] holds OURO_CTR_SHARDS copies of the 2K + OURO_CTR_N counters (by SM). */

@@ -1136,7 +1136,11 @@ __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k,
             u64 g0 = 0, g1 = 0;
             if (p0) g0 = ~atomicOr(row + wi, p0) & p0;
             if (p1) g1 = ~atomicOr(row + wi + 1, p1) & p1;
-            if (g0 != p0 || g1 != p1) raise_err(v, OURO_ERR_CORRUPTION);
+            // A bit another holder took since our load is contention, not corruption:
+            // holders reserve on free_count before claiming (cq_alloc), so the bitmap
+            // always has enough clear bits for every reservation and a rescan finds them.
+            const u32 lost = __ballot_sync(mask, g0 != p0 || g1 != p1);
+            if (lost && lane == __ffs(lost) - 1) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_CLAIM_RETRY), 1ull);
             const u32 gc = (u32)(__popcll((long long)g0) + __popcll((long long)g1));
             u32 gpre, gtot;
             ballot_scan8(mask, gc, lt, &gpre, &gtot);
@@ -1286,9 +1290,11 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             oldfree = __shfl_sync(mask, oldfree, leader);
             if (!take) continue;
             const u32 page = warp_claim(v, c, k, take, mask, lane, (intodo && rank < take) ? rank : NONE);
-            // in-transit rule: the holder puts its entry back.  It cannot overflow the
-            // queue -- our own dequeue freed a ring position and its count -- so the count
-            // update is a fire-and-forget add instead of a capacity-checked RMW round trip.
+            // in-transit rule: the holder puts its entry back.  It cannot
+            // overflow the queue -- our own dequeue freed a ring position and its count
+            // -- so the count update is a fire-and-forget add instead of a
+            // capacity-checked RMW round trip.  (Putting it back before the claim, so
+            // other warps can claim in the chunk meanwhile, measured ~2 % slower.)
             q_enqueue<FL>(v, k, mask, lane, (oldfree - take > 0) ? (1u << leader) : 0u, e, true);
             if (intodo && rank < take) {
                 if (page != NONE) {

@@ -556,6 +556,7 @@ struct orc_heap {
     void build();
     // chunk bitmap primitives
     u32 claim_lowest(u32 c, u32 k, u32 take, u32* pages);
+    u64 claim_collisions = 0;  // bitmap picks lost to a concurrent holder (retried)
     // allocation
     void alloc_class(u32 k, Lane** lanes, u32 n);
     void alloc_page(u32 k, Lane** lanes, u32 n);
@@ -673,8 +674,11 @@ u32 orc_heap::claim_lowest(u32 c, u32 k, u32 take, u32* pages) {
             }
             if (!pick) continue;
             const u64 old = A(bm(c)[w]).fetch_or(pick, AR);
+            // Bits another holder took between our snapshot and the fetch-OR are
+            // contention, not corruption ("retry on contention"): every
+            // holder reserved its pages on free_count first, so the rescan finds ours.
             u64 mine = ~old & pick;
-            if (mine != pick) ar.err.raise(OURO_ERR_CORRUPTION);
+            if (mine != pick) A(claim_collisions).fetch_add(1, RLX);
             while (mine) {
                 pages[got++] = w * 64 + (u32)std::countr_zero(mine);
                 mine &= mine - 1;
