@@ -471,15 +471,24 @@ __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_
     return (r & 1u) != 0;
 }
 
-// Did this block recently see the queue empty?  (hint only: it just turns the
-// first try's RMW into observe-then-RMW, which reserves exactly the same.)  A
-// pump active in this block is the freshest evidence.
+// Did this block see the queue empty lately?  A pump active in this block (its
+// latest poll) is the freshest evidence, else a hint at most kPollWindow old --
+// this block's failed RMWs and pump terms, or seeded from the SM's (block start).
+// Then the call's first try fails on that observation instead of an RMW + undo
+// pair per warp (the retry rounds that follow each make a fresh observation, so
+// OutOfMemory still takes max_retries of them).  With
+// OURO_FIRST_TRY_OBSERVE=1 the try is a block-combined poll issued after the call
+// began instead (measured: ~3 us per warp at the start of each OOM-storm wave, the
+// block's warps polling one after another).
+#ifndef OURO_FIRST_TRY_OBSERVE
+#define OURO_FIRST_TRY_OBSERVE 0
+#endif
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
     const u64 o = ld_sh(poll_slot(tag));
     if (tag_is(o, tag) && (o & kPump)) return (o & 1u) != 0;
     const u64 e = ld_sh(hint_slot(tag));
-    return tag_is(e, tag) && (e & 1u) && time_recent(gtime32(), e, 4 * kPollWindow);
+    return tag_is(e, tag) && (e & 1u) && time_recent(gtime32(), e, kPollWindow);
 }
 // A reservation RMW issued at tick t0 found the queue empty: record the hint.
 __device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u32 t0, u64* smh) {
@@ -505,7 +514,11 @@ __device__ __forceinline__ u32 reserve_deq(const ouro_heap_view& v, ouro_queue_d
             return 0;
         }
     } else if (hint_empty(Q)) {
+#if OURO_FIRST_TRY_OBSERVE
         if (observe_once(Q, floor, sm_hint_row(v))) return 0;
+#else
+        return 0;
+#endif
     }
     const u32 t0 = gtime32();
     OURO_DBG(7, 1);
