@@ -531,7 +531,16 @@ __device__ __forceinline__ u32 reserve_deq(const ouro_heap_view& v, ouro_queue_d
     }
     return got;
 }
+// An enqueue by this block makes its "empty" hint for Q wrong: drop it, so a first
+// try of this block does not fail on it (a single warp that frees and allocates
+// again behaves exactly like the oracle's group operations).
+__device__ __forceinline__ void clear_hint(const ouro_queue_dev* Q) {
+    const u64 tag = poll_tag(Q);
+    u64* h = hint_slot(tag);
+    if (tag_is(ld_sh(h), tag)) *reinterpret_cast<volatile u64*>(h) = 0;
+}
 __device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
+    clear_hint(Q);
     const i64 old = (i64)atomicAdd((u64*)&Q->count, (u64)n);
     if (old + (i64)n > (i64)Q->cap) { atomicAdd((u64*)&Q->count, (u64)(-(i64)n)); return false; }
     return true;
@@ -542,6 +551,7 @@ __device__ __forceinline__ bool reserve_enq(ouro_queue_dev* Q, u32 n) {
 // and pools hold each chunk at most once): fire-and-forget add, no round trip.
 __device__ __forceinline__ void reserve_enq_nofull(ouro_queue_dev* Q, u32 n) {
     atomicAdd((u64*)&Q->count, (u64)n);
+    clear_hint(Q);
 }
 
 // Tag of a filled virtual-queue slot: the segment's sequence number (each slot
