@@ -276,10 +276,11 @@ def rmw_per_pair(kind, flavor, size, chunk=64 << 10):
 
 
 def _traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/r1c_traffic.json): the 16 B launch, where all threads are served."""
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    capture of the current tree (profiles/r2_traffic.json): the 16 B alloc launch,
+    where every thread is served (8.6 MB against 8.4 MB of algorithmic slot reads)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1c_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
             return json.load(f)["per_launch_dram_bytes"]["16"]
     except Exception:
         return None
