@@ -483,10 +483,21 @@ __device__ __forceinline__ bool fail_rounds(const ouro_heap_view& v, ouro_queue_
 #ifndef OURO_FIRST_TRY_OBSERVE
 #define OURO_FIRST_TRY_OBSERVE 0
 #endif
+#ifndef OURO_HINT_PUMP
+#define OURO_HINT_PUMP 1
+#endif
+#ifndef OURO_POOL_HINT_SKIP
+#define OURO_POOL_HINT_SKIP 1  // chunk-kind pool first tries fail on a recent empty hint (0: observe first)
+#endif
+#ifndef OURO_CQ_CLASS_HINT
+#define OURO_CQ_CLASS_HINT 1   // chunk-kind class queue first tries: 0 ignore hints, 1 observe on a hint
+#endif
 __device__ __forceinline__ bool hint_empty(const ouro_queue_dev* Q) {
     const u64 tag = poll_tag(Q);
+#if OURO_HINT_PUMP
     const u64 o = ld_sh(poll_slot(tag));
     if (tag_is(o, tag) && (o & kPump)) return (o & 1u) != 0;
+#endif
     const u64 e = ld_sh(hint_slot(tag));
     return tag_is(e, tag) && (e & 1u) && time_recent(gtime32(), e, kPollWindow);
 }
@@ -505,20 +516,24 @@ __device__ __forceinline__ void note_empty(const ouro_queue_dev* Q, u32 t0, u64*
 // starts with a block-combined observation issued after the call began (an OOM
 // storm costs one count load per block, not an RMW + undo pair per warp); a
 // non-empty answer still goes through the RMW, which decides.
+// `hint_skip`: on a recent "empty" hint the try fails without an RMW (page-kind
+// class queues, the pool); false: the hint only triggers a fresh block-combined
+// observation first (chunk-kind class queues: empty whenever their few entries are
+// in transit, so a hint would send served requests to the pool).
 __device__ __forceinline__ u32 reserve_deq(const ouro_heap_view& v, ouro_queue_dev* Q, u32 n, i64 floor,
-                                           bool precheck = true, bool combine = false) {
+                                           bool precheck = true, bool combine = false, bool hint_skip = true) {
     if (precheck) {
         if (combine) {
             if (observed_empty(Q, floor, sm_hint_row(v))) return 0;
         } else if ((i64)ld_rlx((const u64*)&Q->count) - floor <= 0) {
             return 0;
         }
-    } else if (hint_empty(Q)) {
-#if OURO_FIRST_TRY_OBSERVE
-        if (observe_once(Q, floor, sm_hint_row(v))) return 0;
-#else
-        return 0;
-#endif
+    } else if ((hint_skip || OURO_CQ_CLASS_HINT) && hint_empty(Q)) {
+        if (!hint_skip || OURO_FIRST_TRY_OBSERVE) {
+            if (observe_once(Q, floor, sm_hint_row(v))) return 0;
+        } else {
+            return 0;
+        }
     }
     const u32 t0 = gtime32();
     OURO_DBG(7, 1);
@@ -613,12 +628,12 @@ __device__ __forceinline__ bool arr_enqueue(const ouro_heap_view& v, ouro_queue_
 // served; the `got` lowest-ranked lanes of todo get *val (NONE on timeout).
 __device__ __forceinline__ u32 arr_dequeue(const ouro_heap_view& v, ouro_queue_dev* Q, u32 mask,
                                            u32 lane, u32 todo, i64 floor, u32* val, bool precheck = true,
-                                           bool combine = false) {
+                                           bool combine = false, bool hint_skip = true) {
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(v, Q, n, floor, precheck, combine);
+        got = reserve_deq(v, Q, n, floor, precheck, combine, hint_skip);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -1050,14 +1065,15 @@ __device__ __forceinline__ bool q_enqueue(const ouro_heap_view& v, u32 qi, u32 m
 // Warp-collective dequeue for the lanes of `todo` (all on queue `qi`).
 template <int FL>
 __device__ __forceinline__ u32 q_dequeue(const ouro_heap_view& v, u32 qi, u32 mask, u32 lane, u32 todo,
-                                         i64 floor, u32* val, bool precheck = true, bool combine = false) {
+                                         i64 floor, u32* val, bool precheck = true, bool combine = false,
+                                         bool hint_skip = true) {
     ouro_queue_dev* Q = v.q + qi;
-    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val, precheck, combine);
+    if (FL == FL_ARRAY) return arr_dequeue(v, Q, mask, lane, todo, floor, val, precheck, combine, hint_skip);
     const u32 leader = __ffs(todo) - 1, n = __popc(todo), rank = __popc(todo & lanemask_lt());
     u32 got = 0;
     u64 t0 = 0;
     if (lane == leader) {
-        got = reserve_deq(v, Q, n, floor, precheck, combine);
+        got = reserve_deq(v, Q, n, floor, precheck, combine, hint_skip);
         if (got) t0 = atomicAdd((u64*)&Q->head, (u64)got);
     }
     got = __shfl_sync(mask, got, leader);
@@ -1291,7 +1307,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
         const bool intodo = (todo >> lane) & 1u;
         u32 e = NONE;
         // first try: straight to the RMW unless this block saw the queue empty (hinted)
-        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0);
+        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0, false);
         e = __shfl_sync(mask, e, leader);
         if (got && e != NONE) {
             const u32 c = e & v.cmask;
@@ -1331,7 +1347,8 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             continue;
         }
         u32 c = NONE;
-        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, attempt > 0, attempt > 0);
+        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, attempt > 0, attempt > 0,
+                          OURO_POOL_HINT_SKIP);
         c = __shfl_sync(mask, c, leader);
         if (got && c != NONE) {
             const u32 take = min(n, ppc);
