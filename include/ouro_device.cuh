@@ -237,12 +237,8 @@ __device__ __forceinline__ u64 mk_obs(u32 seq, u64 tag, u32 flags, u32 streak) {
 #if OURO_STORM_STATS
 __device__ unsigned long long g_storm_dbg[256 * 32];
 #define OURO_DBG(i, x) atomicAdd(&g_storm_dbg[(sm_id() & 255u) * 32u + (i)], (unsigned long long)(x))
-struct StormLocal { unsigned long long c[16]; };
-#define OURO_LDBG(L, i, x) ((L) ? (void)((L)->c[i] += (x)) : (void)0)
 #else
 #define OURO_DBG(i, x) ((void)0)
-#define OURO_LDBG(L, i, x) ((void)0)
-struct StormLocal { unsigned long long c[1]; };
 #endif
 constexpr u64 kPump = 2u;
 constexpr u32 kPoolEmpty = 4u;
@@ -316,10 +312,8 @@ __device__ __forceinline__ u32 obs_need(u64* slot, u64 tag) {
 // replaced a stalled pump is simply overwritten).  Returns the poll's flag bits
 // (bit 0 = empty).
 __device__ __forceinline__ u32 obs_round(ouro_queue_dev* Q, i64 floor, ouro_queue_dev* P, i64 pfloor, u64* slot,
-                                         u64 tag, u32* need, u64* pumpv, StormLocal* SL = nullptr) {
-    (void)SL;
+                                         u64 tag, u32* need, u64* pumpv) {
     if (*pumpv) {
-        OURO_LDBG(SL, 2, 1);
         const u32 fl = poll_load(Q, floor, P, pfloor);
         const u32 s = e_seq(*pumpv) + 1u;
         const u64 nv = mk_obs(s, tag, (u32)kPump | fl, (fl & 1u) ? e_streak(*pumpv) + 1u : 0u);
@@ -332,7 +326,6 @@ __device__ __forceinline__ u32 obs_round(ouro_queue_dev* Q, i64 floor, ouro_queu
         const u64 e = ld_sh(slot);
         const bool mine = tag_is(e, tag);
         if (mine && (int)(e_seq(e) - *need) >= 0) {  // another warp's poll, new enough
-            OURO_LDBG(SL, 3, 1);
             *need = e_seq(e) + 1u;
             return (u32)e & (1u | kPoolEmpty);
         }
@@ -342,13 +335,10 @@ __device__ __forceinline__ u32 obs_round(ouro_queue_dev* Q, i64 floor, ouro_queu
             if (spins < kPumpSteal) continue;
         }
         // no pump (or it stalled): poll, publish, take the role
-        OURO_LDBG(SL, 2, 1);
-        OURO_LDBG(SL, 4, 1);
         const u32 fl = poll_load(Q, floor, P, pfloor);
         const u32 s = mine ? e_seq(e) + 1u : *need;
         const u64 nv = mk_obs(s, tag, (u32)kPump | fl, (fl & 1u) ? (mine && (e & 1u) ? e_streak(e) + 1u : 1u) : 0u);
         *pumpv = atomicCAS(slot, e, nv) == e ? nv : 0;  // lost: someone published first; ours stays private
-        OURO_LDBG(SL, 10, *pumpv ? 0 : 1);
         *need = s + 1u;
         return fl;
     }
@@ -398,9 +388,20 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
     const u64 tag = poll_tag(Q);
     u64* slot = PAIR ? pair_slot(tag) : poll_slot(tag);
     u32 need = obs_need(slot, tag), fl = 1u, seq = 0, streak = 0, extra = 0;
+#if OURO_STORM_STATS
+    const u64 c0 = clock64();
+    const u32 a0 = a;
+    OURO_DBG(0, 1);
+#endif
     // Waiting rounds: take the pump's polls, or claim the role when there is no pump.
     for (;;) {
-        if (++a >= maxr) return (a << 1) | 1u;
+        if (++a >= maxr) {
+#if OURO_STORM_STATS
+            OURO_DBG(1, a - a0);
+            OURO_DBG(11, clock64() - c0);
+#endif
+            return (a << 1) | 1u;
+        }
         backoff_policy(SLEEP ? (u32)OURO_BACKOFF_SLEEP : (u32)OURO_BACKOFF_FENCE, base_ns, cap_ns, a);
         // FenceRetry: a round may take a poll the pump made while this warp was
         // still on an earlier round -- each such poll is newer than the previous
@@ -428,8 +429,17 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
             poll_wait();
         }
         if (claimed) break;
-        if (!(fl & 1u)) return a << 1;
+        if (!(fl & 1u)) {
+#if OURO_STORM_STATS
+            OURO_DBG(1, a - a0);
+            OURO_DBG(11, clock64() - c0);
+#endif
+            return a << 1;
+        }
     }
+#if OURO_STORM_STATS
+    const u32 ap = a;
+#endif
     // Pump rounds: poll back to back (this round's poll first).  Unrolled: ptxas
     // puts a YIELD at the head of a loop whose exit depends on a loaded value, and
     // a yield per round cost the pump ~350 cycles with the SM's other warps ready
@@ -450,6 +460,11 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
         if (!(fl & 1u)) { r = a << 1; break; }
     }
     *reinterpret_cast<volatile u64*>(slot) = mk_obs(seq, tag, fl, streak);  // release: the last poll stays readable
+#if OURO_STORM_STATS
+    OURO_DBG(1, a - a0);
+    OURO_DBG(14, a - ap + 1);
+    OURO_DBG(11, clock64() - c0);
+#endif
     // seed the hints of blocks that start later on this SM (one store per pump term)
     if (PAIR) publish_hint(smh, poll_tag(P), mk_entry(gtime32(), poll_tag(P), (fl & kPoolEmpty) ? 1u : 0u));
     else publish_hint(smh, tag, mk_entry(gtime32(), tag, fl & 1u));

@@ -9,8 +9,8 @@ import torch
 
 import paper_2504_18211_b200 as ob
 
-NAMES = ["round loops", "rounds", "polls", "taken from pump", "polls as non-pump", "observe_once", "poll-load cycles", "reserve RMWs",
-         "wait spins", "spins per taken(all)", "lost publish CAS", "round-loop cycles", "fence cycles", "obs cycles", "pump rounds", "pump round cycles"]
+NAMES = ["round loops", "rounds", "-", "-", "-", "observe_once", "-", "reserve RMWs", "-", "-", "-",
+         "round-loop cycles", "-", "-", "pump rounds"]
 size = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 kind = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 n = 1 << 20
@@ -28,10 +28,7 @@ with ob.Heap(ob.HeapConfig(1 << 30, allocator_kind=ob.AllocatorKind(kind))) as h
               "  ".join(f"{nm}={out[i]}" for i, nm in enumerate(NAMES) if nm != "-"))
         if out[1]:
             print(f"   cycles/round {out[11] / out[1]:.0f}  rounds/loop {out[1] / max(out[0], 1):.1f}  "
-                  f"polls/round {out[2] / out[1]:.3f}  spins/taken {out[8] / max(out[3], 1):.1f}  "
-                  f"fence/round {out[12] / out[1]:.0f}  obs/round {out[13] / out[1]:.0f}  "
-                  f"poll-load {out[6] / max(out[2], 1):.0f} cyc  all-spins/taken {out[9] / max(out[3], 1):.1f}  "
-                  f"pump-round {out[15] / max(out[14], 1):.0f} cyc ({out[14] / out[1]:.3f} of rounds)")
+                  f"pump share of rounds {out[14] / out[1]:.3f}")
         if out[16]:
             print(f"   per OOM warp: pq_alloc->rounds {out[17] / out[16]:.0f} cyc, rounds {out[18] / out[16]:.0f} cyc, "
                   f"after {out[19] / out[16]:.0f} cyc;  per warp: block_init {out[21] / out[20]:.0f} cyc, "
