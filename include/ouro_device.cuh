@@ -252,20 +252,8 @@ __device__ __forceinline__ void poll_wait() {
     __nanosleep(OURO_POLL_WAIT_NS);
 #endif
 }
-// Block shared state: [0,16) observations, [16,32) hints, [32,48) pair
-// observations, then the chunk-kind block fetch state (cq_alloc_block): per
-// class a fetch flag and a waiting-warps mask, per warp a slot owner, a request
-// and a grant; last, the magic ouro_block_init() writes.
-constexpr u32 kFetchAt = 3 * kPollEntries;  // u32[16]
-constexpr u32 kWaitAt = kFetchAt + 8;       // u32[16]
-constexpr u32 kOwnAt = kWaitAt + 8;         // u32[32]
-constexpr u32 kReqAt = kOwnAt + 16;         // u32[32]
-constexpr u32 kGrantAt = kReqAt + 16;       // u64[32]
-constexpr u32 kMagicAt = kGrantAt + 32;
-constexpr u32 kBlockWords = kMagicAt + 1;
-constexpr u64 kBlockMagic = 0x4F55524F424C4B32ull;
 __device__ __forceinline__ u64* poll_cache() {
-    __shared__ u64 cache[kBlockWords];
+    __shared__ u64 cache[3 * kPollEntries];  // [0,16) observations, [16,32) hints, [32,48) pair observations
     return cache;
 }
 // Queue structs are laid out consecutively, so the struct index is a collision-free
@@ -1169,24 +1157,13 @@ __device__ __forceinline__ void q_enqueue_by_queue(const ouro_heap_view& v, u32 
 // (lowest free word first, fetch-OR the chosen bits).
 // Each lane of `mask` scans two words per window; the requester of rank
 // `req` (< take, NONE for others) receives the req-th lowest claimed page.
-//
-// `oldfree`: the header's free count the caller's reservation started from (0 =
-// unknown).  Holders that reserved before us and have not claimed yet own
-// (free bits seen) - oldfree of the lowest free pages, so our first pass skips
-// that many and takes the next `take`: concurrent holders of one chunk claim
-// disjoint bits instead of all racing for the lowest word.  With no other
-// holder the skip is 0 -- the lowest free pages, as the oracle takes them.  The
-// skip is a hint (a free in flight can shift it); a short first pass and every
-// later pass take the lowest free bits.
 __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k, u32 take, u32 mask,
-                                          u32 lane, u32 req, u32 oldfree = 0) {
+                                          u32 lane, u32 req) {
     const u32 L = __popc(mask), lt = lanemask_lt(), li = __popc(mask & lt);
     const u32 W = words_of(v, k);
     const u32 ppc = ppc_of(v, k);
     u64* row = bm_row(v, c);
     u32 claimed = 0, page = NONE;
-    // the skip needs the whole bitmap in one window
-    bool first = oldfree != 0 && W <= 2 * L;
     Spin sp;
     while (claimed < take) {
         for (u32 wb = 0; wb < W && claimed < take; wb += 2 * L) {
@@ -1206,23 +1183,10 @@ __device__ __forceinline__ u32 warp_claim(const ouro_heap_view& v, u32 c, u32 k,
             u32 pre, tot;
             ballot_scan8(mask, cnt, lt, &pre, &tot);
             const u32 need = take - claimed;
-            const u32 skip = (first && tot > oldfree) ? tot - oldfree : 0u;
-            first = false;
-            // this lane's free bits have ranks [pre, pre + cnt); ours are [skip, skip + need)
-            const u32 lo = max(pre, skip), hi = min(pre + cnt, skip + need);
-            u32 my = hi > lo ? hi - lo : 0u;
-            u32 sk = my ? lo - pre : 0u;
+            u32 my = pre >= need ? 0u : min(cnt, need - pre);
             u64 p0 = 0, p1 = 0;
-            for (u64 b = w0; my && b; b &= b - 1) {
-                if (sk) { --sk; continue; }
-                p0 |= b & (~b + 1);
-                --my;
-            }
-            for (u64 b = w1; my && b; b &= b - 1) {
-                if (sk) { --sk; continue; }
-                p1 |= b & (~b + 1);
-                --my;
-            }
+            for (u64 b = w0; my && b; b &= b - 1, --my) p0 |= b & (~b + 1);
+            for (u64 b = w1; my && b; b &= b - 1, --my) p1 |= b & (~b + 1);
             u64 g0 = 0, g1 = 0;
             if (p0) g0 = ~atomicOr(row + wi, p0) & p0;
             if (p1) g1 = ~atomicOr(row + wi + 1, p1) & p1;
@@ -1343,265 +1307,6 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
 #endif
 }
 
-// ---- chunk kind: block fetch ------------------------------------------------
-// Under load every warp of every block allocating in class k dequeues one of the
-// class queue's few entries, reserves pages with a CAS on that chunk's header and
-// puts the entry back: four RMWs on a handful of hot words per warp,
-// serialized at their L2 slices.  Here the warps of one block pool their
-// requests: the warps waiting in class k register (request = lanes, bit in the
-// class's waiting mask); one of them, holding the class's fetch flag, takes the
-// mask, dequeues ONE entry, reserves pages for all of them with ONE header CAS
-// and writes each warp a grant -- (chunk entry, count) to claim in the bitmap,
-// or, for a chunk fresh from the pool whose pages it marked itself, (chunk,
-// first page, count) -- then clears the flag.  Each warp claims its own pages,
-// in parallel; the fetcher puts the entry back after its own claim.  The hot
-// words see one RMW per block fetch instead of one per warp.  With a single
-// warp the fetch is the plain protocol step for step (the single-warp parity
-// scripts), so the oracle's restatement covers it unchanged.
-#ifndef OURO_CLAIM_SKIP
-#define OURO_CLAIM_SKIP 1
-#endif
-#ifndef OURO_CQ_BLOCK
-#define OURO_CQ_BLOCK 0
-#endif
-#ifndef OURO_BLOCK_WAIT_NS
-#define OURO_BLOCK_WAIT_NS 0      // > 0: a waiting warp sleeps between checks
-#endif
-constexpr u64 kGrantValid = 1ull << 63;
-constexpr u32 kGrantRetry = 0, kGrantClaim = 1, kGrantDirect = 2, kGrantEmpty = 3;
-__device__ __forceinline__ u64 mk_grant(u32 type, u32 cnt, u32 basepg, u32 word) {
-    return kGrantValid | ((u64)type << 60) | ((u64)basepg << 38) | ((u64)cnt << 32) | word;
-}
-__device__ __forceinline__ u32 g_type(u64 g) { return (u32)(g >> 60) & 3u; }
-__device__ __forceinline__ u32 g_cnt(u64 g) { return (u32)(g >> 32) & 63u; }
-__device__ __forceinline__ u32 g_base(u64 g) { return (u32)(g >> 38) & 0x3FFFFFu; }
-__device__ __forceinline__ u32* bs32(u32 at) { return reinterpret_cast<u32*>(poll_cache() + at); }
-__device__ __forceinline__ u32* fetch_flag(u32 k) { return bs32(kFetchAt) + (k & 15); }
-__device__ __forceinline__ u32* wait_mask(u32 k) { return bs32(kWaitAt) + (k & 15); }
-__device__ __forceinline__ u32* own_slot(u32 w) { return bs32(kOwnAt) + (w & 31); }
-__device__ __forceinline__ u32* req_slot(u32 w) { return bs32(kReqAt) + (w & 31); }
-__device__ __forceinline__ u64* grant_slot(u32 w) { return poll_cache() + kGrantAt + (w & 31); }
-__device__ __forceinline__ u32 ld_sh32(const u32* p) { return *reinterpret_cast<const volatile u32*>(p); }
-__device__ __forceinline__ void st_sh64(u64* p, u64 x) { *reinterpret_cast<volatile u64*>(p) = x; }
-__device__ __forceinline__ u32 warp_in_block() {
-    return (threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z)) >> 5;
-}
-__device__ __forceinline__ bool block_ready() { return ld_sh(poll_cache() + kMagicAt) == kBlockMagic; }
-
-// Leader lane: register `n` lanes and wait for a grant or the fetch flag.
-// Returns the grant, or 0 = this warp now holds the flag and fetches.
-__device__ __forceinline__ u64 block_wait(const ouro_heap_view& v, u32 k, u32 w, u32 n) {
-    *reinterpret_cast<volatile u32*>(req_slot(w)) = n;
-    st_sh64(grant_slot(w), 0ull);
-    __threadfence_block();
-    atomicOr(wait_mask(k), 1u << w);
-    const long long t0 = clock64();
-    for (;;) {
-        u64 g = ld_sh(grant_slot(w));
-        if (g) return g;
-        if (ld_sh32(fetch_flag(k)) == 0u && atomicCAS(fetch_flag(k), 0u, 1u) == 0u) {
-            __threadfence_block();
-            g = ld_sh(grant_slot(w));  // a fetcher that just finished may have served us
-            if (g) { atomicExch(fetch_flag(k), 0u); return g; }
-            return 0;
-        }
-#if OURO_BLOCK_WAIT_NS > 0
-        __nanosleep(OURO_BLOCK_WAIT_NS);
-#endif
-        if (clock64() - t0 > (1ll << 31)) {  // ~1 s: a fetcher never came back
-            raise_err(v, OURO_ERR_TIMEOUT);
-            atomicAnd(wait_mask(k), ~(1u << w));
-            return mk_grant(kGrantEmpty, 0, 0, 0);
-        }
-    }
-}
-// Leader lane: write each waiting warp of `set` its share of `T` pages (ascending
-// warp order), mode `type`; returns `w`'s own grant.  Clears the fetch flag.
-// Claim grants carry the free count their share starts from (warp_claim's skip
-// hint; 0 = none), direct grants their first page.
-__device__ __forceinline__ u64 block_grant(u32 k, u32 w, u32 set, u32 type, u32 T, u32 word, u32 oldfree = 0) {
-    u32 given = 0;
-    u64 mine = 0;
-    for (u32 s = set; s; s &= s - 1) {
-        const u32 x = __ffs(s) - 1;
-        const u32 gx = min(ld_sh32(req_slot(x)), T - given);
-        const u32 f = oldfree - given;
-        const u32 b = type == kGrantClaim ? (f < (1u << 22) ? f : 0u) : given;
-        const u64 g = gx ? mk_grant(type, gx, b, word) : mk_grant(kGrantRetry, 0, 0, 0);
-        given += gx;
-        if (x == w) mine = g;
-        else st_sh64(grant_slot(x), g);
-    }
-    __threadfence_block();
-    atomicExch(fetch_flag(k), 0u);
-    return mine;
-}
-
-// The warp holding class k's fetch flag: serve every registered warp of the
-// block with one dequeue (or one pool chunk).  Returns this warp's own grant;
-// *put = the entry the caller puts back after its claim (NONE: none).
-template <int FL>
-__device__ __forceinline__ u64 block_fetch(const ouro_heap_view& v, u32 k, u32 w, u32 mask, u32 lane, u32 leader,
-                                           u32 attempt, u32* put) {
-    const u32 ppc = ppc_of(v, k);
-    const u32 pool = v.K;
-    // The waiting set is taken once the entry (or pool chunk) is in hand, so the
-    // warps that registered during the dequeue's round trips are served too.
-    u32 set = 1u << w, need = 0;
-    auto snap = [&]() {
-        set |= atomicExch(wait_mask(k), 0u);
-        need = 0;
-        for (u32 s = set; s; s &= s - 1) need += ld_sh32(req_slot(__ffs(s) - 1));
-    };
-    *put = NONE;
-    for (;;) {
-        u32 e = NONE;
-        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0, false);
-        e = __shfl_sync(mask, e, leader);
-        if (got && e != NONE) {
-            const u32 c = e & v.cmask;
-            const u32 glow = v.chunk_bits >= 32 ? 0u : (e >> v.chunk_bits);
-            u64 mine = 0;
-            u32 take = 0, oldfree = 0;
-            if (lane == leader) {
-                snap();
-                u64 m = ld_rlx(v.meta + c);
-                for (;;) {
-                    if (m_state(m) != k + 1 || (m_gen(m) & v.gmask) != glow || m_free(m) == 0) break;
-                    const u32 f = m_free(m);
-                    const u32 t = min(need, f);
-                    const u64 prev = atomicCAS(v.meta + c, m, m - t);
-                    if (prev == m) { take = t; oldfree = f; break; }
-                    m = prev;
-                }
-                if (!take) atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_STALE), 1ull);
-                else mine = block_grant(k, w, set, kGrantClaim, take, e, OURO_CLAIM_SKIP ? oldfree : 0u);
-            }
-            take = __shfl_sync(mask, take, leader);
-            if (!take) continue;  // stale entry dropped: dequeue again for the same set
-#if OURO_STORM_STATS
-            if (lane == leader) { OURO_DBG(25, 1); OURO_DBG(26, __popc(set)); OURO_DBG(27, need - take > 0 ? 1 : 0); }
-#endif
-            oldfree = __shfl_sync(mask, oldfree, leader);
-            if (oldfree > take) *put = e;
-            return shfl64(mask, mine, leader);
-        }
-        u32 c = NONE;
-        got = arr_dequeue(v, v.q + pool, mask, lane, 1u << leader, v.floor_F, &c, attempt > 0, attempt > 0,
-                          OURO_POOL_HINT_SKIP);
-        c = __shfl_sync(mask, c, leader);
-        if (got && c != NONE) {
-            u64 m = 0;
-            if (lane == leader) {
-                atomicAdd(ctr_at(v, 2 * v.K + OURO_CTR_POOL_DEQ), 1ull);
-                snap();
-                m = ld_rlx(v.meta + c);
-            }
-            const u32 take = min(__shfl_sync(mask, need, leader), ppc);
-            m = shfl64(mask, m, leader);
-            if (m_state(m) != ST_UNASSIGNED) {
-                if (lane == leader) raise_err(v, OURO_ERR_CORRUPTION);
-                continue;
-            }
-            const u32 gen = (m_gen(m) + 1u) & 0xFFFFFFu;
-#if OURO_STORM_STATS
-            if (lane == leader) { OURO_DBG(28, 1); OURO_DBG(26, __popc(set)); }
-#endif
-            // chunk_assign fused with taking pages 0..take-1 (cq_alloc below): the
-            // pool chunk's bitmap is all-zero, the header is published after the
-            // bitmap RMWs returned, the entry enqueued after the header.
-            u64 mine = 0;
-            if (lane == leader) {
-                for (u32 b = 0; b < take; b += 64) {
-                    const u32 nb = min(64u, take - b);
-                    const u64 tb = (nb >= 64) ? ~0ull : ((1ull << nb) - 1ull);
-                    if (atomicOr(bm_row(v, c) + (b >> 6), tb) & tb) raise_err(v, OURO_ERR_CORRUPTION);
-                }
-                const u64 prev = atomicExch(v.meta + c, mk_meta(gen, k + 1, ppc - take));
-                if (m_state(prev) != ST_UNASSIGNED) raise_err(v, OURO_ERR_CORRUPTION);
-                atomicAdd(v.assigned + k, 1u);
-                mine = block_grant(k, w, set, kGrantDirect, take, c);
-            }
-            __syncwarp(mask);
-            q_enqueue<FL>(v, k, mask, lane, (ppc - take > 0) ? (1u << leader) : 0u, q_entry(v, c, gen));
-            return shfl64(mask, mine, leader);
-        }
-        // both empty: every waiting warp runs its own retry rounds (pump-combined)
-        if (lane == leader) {
-            snap();
-            block_grant(k, w, set, kGrantEmpty, 0, 0);
-        }
-        return mk_grant(kGrantEmpty, 0, 0, 0);
-    }
-}
-
-template <int FL>
-__device__ __forceinline__ void cq_alloc_block(const ouro_heap_view& v, u32 k, u32 gm, u32 mask, u32 lane, u32 w,
-                                               void** res, int* st) {
-    u32 todo = gm, attempt = 0;
-    const u32 lt = lanemask_lt();
-    const u32 pool = v.K;
-    const u32 gl0 = __ffs(gm) - 1;
-    u64 retries = 0;
-#if OURO_STORM_STATS
-    const long long tb0 = clock64();
-#endif
-    while (todo) {
-        const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
-        const bool intodo = (todo >> lane) & 1u;
-        u64 g = 0;
-#if OURO_STORM_STATS
-        const long long tw0 = clock64();
-#endif
-        if (lane == leader) g = block_wait(v, k, w, n);
-        g = shfl64(mask, g, leader);
-#if OURO_STORM_STATS
-        if (lane == leader) { OURO_DBG(30, clock64() - tw0); OURO_DBG(29, g ? 0 : 1); }
-#endif
-        u32 put = NONE;
-        if (!g) g = block_fetch<FL>(v, k, w, mask, lane, leader, attempt, &put);
-        const u32 type = g_type(g), cnt = g_cnt(g);
-        if (type == kGrantClaim || type == kGrantDirect) {
-            const u32 c = (type == kGrantClaim) ? ((u32)g & v.cmask) : (u32)g;
-            const bool mine = intodo && rank < cnt;
-            u32 page = NONE;
-            if (type == kGrantClaim) page = warp_claim(v, c, k, cnt, mask, lane, mine ? rank : NONE, g_base(g));
-            else page = g_base(g) + rank;
-            // the fetcher's in-transit put-back, after its claim; its own
-            // dequeue freed the ring position, so no capacity check (see cq_alloc)
-            if (put != NONE) q_enqueue<FL>(v, k, mask, lane, 1u << leader, put, true);
-            if (mine) {
-                if (page != NONE) {
-                    *res = v.base + ((u64)c << v.chunk_shift) + ((u64)page << (v.min_shift + k));
-                    *st = OURO_OK;
-                } else {
-                    *st = OURO_ERR_CORRUPTION;
-                }
-            }
-            todo &= ~__ballot_sync(mask, mine);
-            continue;
-        }
-        if (put != NONE) q_enqueue<FL>(v, k, mask, lane, 1u << leader, put, true);
-        if (type == kGrantRetry) continue;
-        // both empty: failed rounds on the leader alone until a poll sees work
-        u32 a = attempt, oom = 0;
-        if (lane == leader) oom = fail_rounds(v, v.q + k, v.q + pool, v.floor_F, &a) ? 1u : 0u;
-        a = __shfl_sync(mask, a, leader);
-        oom = __shfl_sync(mask, oom, leader);
-        retries += (u64)n * (a - attempt);
-        attempt = a;
-        if (oom) {
-            if (lane == leader) atomicAdd(ctr_at(v, v.K + k), (u64)n);
-            if (intodo) *st = OURO_ERR_OOM;
-            break;
-        }
-    }
-#if OURO_STORM_STATS
-    if (lane == gl0) { OURO_DBG(31, clock64() - tb0); OURO_DBG(2, 1); }
-#endif
-    if (retries && lane == gl0) atomicAdd(ctr_at(v, k), retries);
-}
-
 // Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).
 template <int FL>
 __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm, u32 mask, u32 lane,
@@ -1611,22 +1316,9 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
     const u32 ppc = ppc_of(v, k);
     const u32 pool = v.K;
     const u32 gl0 = __ffs(gm) - 1;
-#if OURO_CQ_BLOCK
-    {
-        // block fetch when the block called ouro_block_init and no diverged part of
-        // this warp already holds the warp's slot
-        const u32 w = warp_in_block();
-        u32 on = 0;
-        if (lane == gl0) on = (k < 16 && w < 32 && block_ready() && atomicCAS(own_slot(w), 0u, 1u) == 0u) ? 1u : 0u;
-        if (__shfl_sync(mask, on, gl0)) {
-            cq_alloc_block<FL>(v, k, gm, mask, lane, w, res, st);
-            if (lane == gl0) atomicExch(own_slot(w), 0u);
-            return;
-        }
-    }
-#endif
     u64 retries = 0;
 #if OURO_STORM_STATS
+    // per-call timeline of the leader (tools/cq_stats.py)
     const long long tc0 = clock64();
     long long tc = tc0;
     auto lap = [&](int i) { const long long x = clock64(); if (lane == gl0) OURO_DBG(i, x - tc); tc = x; };
@@ -1662,8 +1354,7 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             oldfree = __shfl_sync(mask, oldfree, leader);
             lap(27);
             if (!take) continue;
-            const u32 page = warp_claim(v, c, k, take, mask, lane, (intodo && rank < take) ? rank : NONE,
-                                        OURO_CLAIM_SKIP ? oldfree : 0u);
+            const u32 page = warp_claim(v, c, k, take, mask, lane, (intodo && rank < take) ? rank : NONE);
             lap(28);
             // in-transit rule: the holder puts its entry back.  It cannot
             // overflow the queue -- our own dequeue freed a ring position and its count
@@ -1913,8 +1604,7 @@ __device__ __forceinline__ void* malloc_coalesced_impl(const ouro_heap_view& v, 
 __device__ __forceinline__ void ouro_block_init() {
     const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
-    for (unsigned i = t; i < ouro_dev::kMagicAt; i += nt) ouro_dev::poll_cache()[i] = 0;
-    if (t == 0) ouro_dev::poll_cache()[ouro_dev::kMagicAt] = ouro_dev::kBlockMagic;
+    for (unsigned i = t; i < 3 * ouro_dev::kPollEntries; i += nt) ouro_dev::poll_cache()[i] = 0;
     __syncthreads();
 }
 // Same, and seed the block's hints from the latest observations other blocks on
@@ -1924,8 +1614,7 @@ __device__ __forceinline__ void ouro_block_init(const ouro_heap_view& h) {
     const unsigned t = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
     const unsigned nt = blockDim.x * blockDim.y * blockDim.z;
     u64* cache = poll_cache();
-    for (unsigned i = t; i < kMagicAt; i += nt) cache[i] = 0;
-    if (t == 0) cache[kMagicAt] = kBlockMagic;
+    for (unsigned i = t; i < 3 * kPollEntries; i += nt) cache[i] = 0;
     __syncthreads();
     const u64* row = sm_hint_row(h);
     if (row) {

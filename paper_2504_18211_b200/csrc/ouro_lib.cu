@@ -221,7 +221,13 @@ __global__ void __launch_bounds__(kBlock) k_free(ouro_heap_view v, u64 n, void* 
 
 __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p) {
     const u64 off = (u64)((const uint8_t*)p - v.base);
-    const u32 st = m_state(v.meta[off >> v.chunk_shift]);
+    const u32 c = (u32)(off >> v.chunk_shift);
+    if (v.kind == KIND_PAGE) {
+        // static partition: the class is arithmetic (as in free_impl), no header load
+        const u32 k = c < v.pq_n0 ? 0u : 1u + (c - v.pq_n0) / v.pq_q;
+        return k < v.K ? 1ull << (v.min_shift + k) : 0ull;
+    }
+    const u32 st = m_state(v.meta[c]);
     if (st == 0 || st > v.K) return 0;
     return 1ull << (v.min_shift + st - 1);
 }
@@ -243,12 +249,21 @@ __device__ __forceinline__ u64 region_len(const ouro_heap_view& v, const void* p
 // lanes in runs of kPatRun consecutive slots (so small regions coalesce per run),
 // the 32 / kPatRun runs of a warp strided Q slots apart over the slot range
 constexpr u32 kPatRun = OURO_PAT_RUN;
+#ifndef OURO_PAT_BATCH
+#define OURO_PAT_BATCH 4
+#endif
+constexpr u32 kPatBatch = OURO_PAT_BATCH;
+// 4 resident blocks (<= 64 registers): the batched verify would otherwise take
+// ~100 registers and run at half the occupancy.
+#ifndef OURO_PAT_MIN_BLOCKS
+#define OURO_PAT_MIN_BLOCKS 4
+#endif
 __device__ __forceinline__ u64 slot_of(u64 g, u32 lane, u64 Q) {
     return g * kPatRun + (lane % kPatRun) + (u64)(lane / kPatRun) * Q;
 }
 template <bool VERIFY>
-__global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, void* const* ptrs, u64 seed, u32 it,
-                                                    u64* result) {
+__device__ __forceinline__ void pattern_body(const ouro_heap_view& v, u64 n, void* const* ptrs, u64 seed, u32 it,
+                                             u64* result) {
     const u32 lane = threadIdx.x & 31;
     const u64 nwarps = ((u64)gridDim.x * blockDim.x) >> 5;
     const u64 runs = 32 / kPatRun;                                        // lane runs per warp
@@ -283,14 +298,26 @@ __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, voi
             const u64 slot = slot_of(g, src, Q);
             const u64 b = pattern_base(seed, slot, it);
             u64 nb = 0;
-            for (u64 j = 2 * lane; j < L / 8; j += 64) {
-                if (VERIFY) {
-                    const ulonglong2 x = reinterpret_cast<const ulonglong2*>(w)[j / 2];
-                    nb += (x.x != pattern_word(b, j)) + (x.y != pattern_word(b, j + 1));
-                } else {
-                    reinterpret_cast<ulonglong2*>(w)[j / 2] =
-                        make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
+            // verify: kPatBatch 512 B steps per pass, all loads issued before the
+            // compares -- that many 16 B loads in flight per lane instead of one
+            // (pq1g 2-8 KiB verify 2.2-2.3 -> 2.8-3.0 TB/s, cq1g 4.3-4.5 -> 5.8-5.9 TB/s;
+            // profiles/r2/pattern_ab.txt).  Stores need no batching.
+            const u64 words = L / 8;
+            if constexpr (VERIFY) {
+                for (u64 j0 = 2 * lane; j0 < words; j0 += 64 * kPatBatch) {
+                    ulonglong2 x[kPatBatch];
+#pragma unroll
+                    for (u32 u = 0; u < kPatBatch; ++u)
+                        if (j0 + 64 * u < words) x[u] = reinterpret_cast<const ulonglong2*>(w)[(j0 + 64 * u) / 2];
+#pragma unroll
+                    for (u32 u = 0; u < kPatBatch; ++u) {
+                        const u64 j = j0 + 64 * u;
+                        if (j < words) nb += (x[u].x != pattern_word(b, j)) + (x[u].y != pattern_word(b, j + 1));
+                    }
                 }
+            } else {
+                for (u64 j = 2 * lane; j < words; j += 64)
+                    reinterpret_cast<ulonglong2*>(w)[j / 2] = make_ulonglong2(pattern_word(b, j), pattern_word(b, j + 1));
             }
             if (VERIFY && nb) { bad += nb; atomicMin(&result[1], slot); }
         }
@@ -299,6 +326,19 @@ __global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, voi
         for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xFFFFFFFFu, bad, o);
         if (lane == 0 && bad) atomicAdd(&result[0], bad);
     }
+}
+// Separate kernels: the verifier is held to 4 resident blocks' registers, the
+// writer compiles to ~40 on its own.
+template <bool VERIFY>
+__global__ void __launch_bounds__(kBlock) k_pattern(ouro_heap_view v, u64 n, void* const* ptrs, u64 seed, u32 it,
+                                                    u64* result) {
+    pattern_body<VERIFY>(v, n, ptrs, seed, it, result);
+}
+template <>
+__global__ void __launch_bounds__(kBlock, OURO_PAT_MIN_BLOCKS) k_pattern<true>(ouro_heap_view v, u64 n,
+                                                                               void* const* ptrs, u64 seed, u32 it,
+                                                                               u64* result) {
+    pattern_body<true>(v, n, ptrs, seed, it, result);
 }
 unsigned pattern_grid(u64 n) { return (unsigned)std::max<u64>(1, ((n + 31) / 32 + 7) / 8); }  // ~one group per warp
 

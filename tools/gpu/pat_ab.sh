@@ -2,7 +2,7 @@
 C=${1:-pq1g}
 for L in $(ls exp/lib_*.so); do
   n=$(basename $L .so)
-  OURO_B200_LIB=$PWD/$L timeout 300 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/pat_${C}_$n.json 2>gpurun_out/pat_${C}_$n.err
+  OURO_B200_LIB=$PWD/$L timeout 300 python bench.py --config $C --steps ${STEPS:-5} --warmup 3 --no-cpu-baseline > gpurun_out/pat_${C}_$n.json 2>gpurun_out/pat_${C}_$n.err
   python - gpurun_out/pat_${C}_$n.json <<'PY'
 import json, sys
 d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
