@@ -364,14 +364,17 @@ def test_virtual_churn_small_segments(cuda, kind, flavor):
         assert d.live_pages == 0 and d.partition_ok == 1
 
 
-@pytest.mark.parametrize("size", [16, 64, 1000, 8192])
-def test_pattern_passes_cover_every_live_region(cuda, size):
+@pytest.mark.parametrize("kind", [0, 1])
+@pytest.mark.parametrize("size", [16, 64, 512, 1000, 2048, 4096, 8192])
+def test_pattern_passes_cover_every_live_region(cuda, size, kind):
     """The write/verify passes must touch every byte of every live region (the
-    passes map slots to lanes in strided runs): write seed 1, verify seed 2 ->
-    every 8-byte word of every live region mismatches; verify seed 1 -> none."""
+    passes map slots to lanes in strided runs; the verifier batches four 512 B
+    steps of a region per pass): write seed 1, verify seed 2 -> every 8-byte word
+    of every live region mismatches; verify seed 1 -> none.  Both kinds: the page
+    kind's region length is partition arithmetic, the chunk kind's the header."""
     torch = cuda
     n = (1 << 18) + 77  # not a multiple of any run width
-    with ob.Heap(_hc(0, 0, 256 << 20)) as h:
+    with ob.Heap(_hc(kind, 0, 256 << 20)) as h:
         ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
         h.launch_alloc(n, ptrs, size=size)
         cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -390,3 +393,31 @@ def test_pattern_passes_cover_every_live_region(cuda, size):
         h.launch_free(n, ptrs)
         torch.cuda.synchronize()
         assert h.last_error()[0] == 0
+
+
+@pytest.mark.parametrize("size,word", [(8192, 3 * 64 + 5), (8192, 1023), (1024, 70), (512, 0), (16, 1)])
+def test_verify_reports_corrupted_words(cuda, size, word):
+    """A word flipped anywhere in a region (any 512 B step of the verifier's batch)
+    is counted once and the lowest corrupted slot is reported."""
+    torch = cuda
+    n = 2048
+    with ob.Heap(_hc(0, 0, 256 << 20)) as h:
+        ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
+        h.launch_alloc(n, ptrs, size=size)
+        h.launch_write(n, ptrs, 7, 1)
+        torch.cuda.synchronize()
+        words = max(16, size) // 8
+        for slot in (1234, 100):
+            p = int(ptrs[slot])
+            assert p != 0
+
+            class Region:
+                __cuda_array_interface__ = {"shape": (words,), "typestr": "<i8", "data": (p, False), "version": 3}
+            r = torch.as_tensor(Region(), device="cuda")
+            r[word] ^= 1
+        res = torch.tensor([0, -1], dtype=torch.int64, device="cuda")
+        h.launch_verify(n, ptrs, 7, 1, res)
+        torch.cuda.synchronize()
+        assert int(res[0]) == 2 and int(res[1]) == 100
+        h.launch_free(n, ptrs)
+        torch.cuda.synchronize()
