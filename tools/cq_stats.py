@@ -1,5 +1,5 @@
 """Per-warp cq_alloc timeline of an OURO_STORM_STATS=1, OURO_CQ_BLOCK=0 build:
-OURO_B200_LIB=exp/lib_cqstats.so python tools/cq_stats.py [size] [flavor] [heap_log2]"""
+OURO_B200_LIB=exp_stats/cqstats.so python tools/cq_stats.py [size] [flavor] [heap_log2] [threads_log2]"""
 import ctypes as C
 import os
 import sys
@@ -12,7 +12,7 @@ import paper_2504_18211_b200 as ob
 size = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 fl = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 heap = 1 << (int(sys.argv[3]) if len(sys.argv) > 3 else 30)
-n = 1 << 20
+n = 1 << (int(sys.argv[4]) if len(sys.argv) > 4 else 20)
 L = ob.lib()
 L.ouro_debug_counters.argtypes = [C.POINTER(C.c_uint64), C.c_int]
 ptrs = torch.zeros(n, dtype=torch.int64, device="cuda")
