@@ -146,6 +146,8 @@ __device__ __forceinline__ void backoff_policy(u32 policy, u32 base_ns, u32 cap_
     } else {
 #if OURO_FENCE_SCOPE_GPU
         asm volatile("fence.sc.gpu;" ::: "memory");
+#elif OURO_FENCE_NONE
+        // measurement builds only: no fence between rounds
 #else
         asm volatile("fence.sc.cta;" ::: "memory");
 #endif
@@ -381,6 +383,9 @@ __device__ __forceinline__ bool observed_empty(ouro_queue_dev* Q, i64 floor, u64
 #define OURO_PUMP_UNROLL 16
 #endif
 constexpr int kPumpUnroll = OURO_PUMP_UNROLL;
+#ifndef OURO_PUMP_PIPELINE
+#define OURO_PUMP_PIPELINE 1
+#endif
 template <bool PAIR, bool SLEEP>
 static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queue_dev* P, i64 pfloor, u32 a,
                                                     u32 maxr, u32 base_ns, u32 cap_ns, u64* smh) {
@@ -444,7 +449,47 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
     // puts a YIELD at the head of a loop whose exit depends on a loaded value, and
     // a yield per round cost the pump ~350 cycles with the SM's other warps ready
     // (tools/rounds_probe.cu: 127 -> 78 us for 2^20 threads x 62 rounds).
+    // Each round's poll is issued as soon as the previous one returned and failed
+    // (and the backoff ran); the previous one is published while the new load is
+    // in flight, so the shared-memory store and the entry arithmetic are off the
+    // poll-to-poll critical path.  (A poll is still issued only after the previous
+    // one completed, and waiters take them in sequence order as before.)
     u32 r;
+#if OURO_PUMP_PIPELINE
+    u64 c0, c1 = 0;
+    c0 = ld_rlx((const u64*)&Q->count);  // this round's poll
+    if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+#pragma unroll kPumpUnroll
+    for (;;) {
+        ++seq;
+        // The entry this poll gets if it finds the queue empty -- the only case that
+        // publishes inside the loop -- does not depend on the loaded value: built
+        // while the load is in flight.
+        const u64 ob = mk_obs(seq, tag, (u32)kPump | 1u | (PAIR ? kPoolEmpty : 0u), streak + 1u);
+        if (PAIR) {
+            const u32 ep = (i64)c1 - pfloor <= 0 ? 1u : 0u;
+            fl = (((i64)c0 <= 0 ? 1u : 0u) & ep) | (ep ? kPoolEmpty : 0u);
+        } else {
+            fl = (i64)c0 <= 0 ? 1u : 0u;
+        }
+        if (!(fl & 1u)) { streak = 0; r = a << 1; break; }
+        ++streak;
+        if (SLEEP) {
+            if (++a >= maxr) { r = (a << 1) | 1u; break; }
+            backoff_policy(OURO_BACKOFF_SLEEP, base_ns, cap_ns, a);
+            c0 = ld_rlx((const u64*)&Q->count);  // next round's poll ...
+            if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+        } else {
+            // FenceRetry: the fence, then the next round's poll, issued before the
+            // budget check (a poll past the budget is simply dropped)
+            backoff_policy(OURO_BACKOFF_FENCE, base_ns, cap_ns, a + 1);
+            c0 = ld_rlx((const u64*)&Q->count);
+            if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+            if (++a >= maxr) { r = (a << 1) | 1u; break; }
+        }
+        *reinterpret_cast<volatile u64*>(slot) = ob;  // ... then this one's entry
+    }
+#else
     bool first = true;
 #pragma unroll kPumpUnroll
     for (;;) {
@@ -459,6 +504,7 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
         *reinterpret_cast<volatile u64*>(slot) = mk_obs(seq, tag, (u32)kPump | fl, streak);
         if (!(fl & 1u)) { r = a << 1; break; }
     }
+#endif
     *reinterpret_cast<volatile u64*>(slot) = mk_obs(seq, tag, fl, streak);  // release: the last poll stays readable
 #if OURO_STORM_STATS
     OURO_DBG(1, a - a0);
