@@ -456,9 +456,9 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
     // one completed, and waiters take them in sequence order as before.)
     u32 r;
 #if OURO_PUMP_PIPELINE
-    u64 c0, c1 = 0;
-    c0 = ld_rlx((const u64*)&Q->count);  // this round's poll
-    if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+    u64 p0, p1 = 0;
+    p0 = ld_rlx((const u64*)&Q->count);  // this round's poll
+    if (PAIR) p1 = ld_rlx((const u64*)&P->count);
 #pragma unroll kPumpUnroll
     for (;;) {
         ++seq;
@@ -467,24 +467,24 @@ static __device__ __noinline__ u32 fail_rounds_loop(ouro_queue_dev* Q, ouro_queu
         // while the load is in flight.
         const u64 ob = mk_obs(seq, tag, (u32)kPump | 1u | (PAIR ? kPoolEmpty : 0u), streak + 1u);
         if (PAIR) {
-            const u32 ep = (i64)c1 - pfloor <= 0 ? 1u : 0u;
-            fl = (((i64)c0 <= 0 ? 1u : 0u) & ep) | (ep ? kPoolEmpty : 0u);
+            const u32 ep = (i64)p1 - pfloor <= 0 ? 1u : 0u;
+            fl = (((i64)p0 <= 0 ? 1u : 0u) & ep) | (ep ? kPoolEmpty : 0u);
         } else {
-            fl = (i64)c0 <= 0 ? 1u : 0u;
+            fl = (i64)p0 <= 0 ? 1u : 0u;
         }
         if (!(fl & 1u)) { streak = 0; r = a << 1; break; }
         ++streak;
         if (SLEEP) {
             if (++a >= maxr) { r = (a << 1) | 1u; break; }
             backoff_policy(OURO_BACKOFF_SLEEP, base_ns, cap_ns, a);
-            c0 = ld_rlx((const u64*)&Q->count);  // next round's poll ...
-            if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+            p0 = ld_rlx((const u64*)&Q->count);  // next round's poll ...
+            if (PAIR) p1 = ld_rlx((const u64*)&P->count);
         } else {
             // FenceRetry: the fence, then the next round's poll, issued before the
             // budget check (a poll past the budget is simply dropped)
             backoff_policy(OURO_BACKOFF_FENCE, base_ns, cap_ns, a + 1);
-            c0 = ld_rlx((const u64*)&Q->count);
-            if (PAIR) c1 = ld_rlx((const u64*)&P->count);
+            p0 = ld_rlx((const u64*)&Q->count);
+            if (PAIR) p1 = ld_rlx((const u64*)&P->count);
             if (++a >= maxr) { r = (a << 1) | 1u; break; }
         }
         *reinterpret_cast<volatile u64*>(slot) = ob;  // ... then this one's entry
