@@ -419,8 +419,13 @@ __device__ __forceinline__ void churn_slot(const ouro_heap_view& v, u64 t, bool 
         if (e) atomicAdd(&res[4], (u64)__popc(e));
     }
 }
+#ifndef OURO_CHURN_MIN_BLOCKS
+#define OURO_CHURN_MIN_BLOCKS 5
+#endif
+// 5 resident blocks (<= 48 registers): left free, the compiler takes 62-64 for the
+// churn loop plus the retry rounds and the kernel loses a fifth of its warps.
 template <int KIND, int FL>
-__global__ void __launch_bounds__(kBlock) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
+__global__ void __launch_bounds__(kBlock, OURO_CHURN_MIN_BLOCKS) k_churn(ouro_heap_view v, u64 n, u32 r, u64 seed, void** slots,
                                                   uint8_t* touched, u64* res) {
     ouro_block_init(v);
     const u64 stride = (u64)gridDim.x * blockDim.x;
