@@ -1353,6 +1353,9 @@ __device__ __forceinline__ void pq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
 #endif
 }
 
+#ifndef OURO_CQ_SKIP_CLASS
+#define OURO_CQ_SKIP_CLASS 1
+#endif
 // Chunk kind, class group `gm` (SPEC.md:261, 299, 206 + G4, 193-197).
 template <int FL>
 __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm, u32 mask, u32 lane,
@@ -1372,13 +1375,23 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
 #else
     auto lap = [](int) {};
 #endif
+    // Set after this call found the class queue empty and then used up a whole pool
+    // chunk (nothing enqueued): its next pages come from the pool without another
+    // class-queue try (classes with fewer pages per chunk than lanes -- 8 KiB: 4
+    // pool chunks per warp -- otherwise pay a class-queue observation per chunk).
+    // A warp alone sees exactly what the try would have seen (an empty queue); a
+    // dry pool sends it back to the class queue before any retry round.
+    bool skip_class = false;
     while (todo) {
         const u32 n = __popc(todo), rank = __popc(todo & lt), leader = __ffs(todo) - 1;
         const bool intodo = (todo >> lane) & 1u;
         u32 e = NONE;
-        // first try: straight to the RMW unless this block saw the queue empty (hinted)
-        u32 got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0, false);
-        e = __shfl_sync(mask, e, leader);
+        u32 got = 0;
+        if (!OURO_CQ_SKIP_CLASS || !skip_class) {
+            // first try: straight to the RMW unless this block saw the queue empty (hinted)
+            got = q_dequeue<FL>(v, k, mask, lane, 1u << leader, 0, &e, attempt > 0, attempt > 0, false);
+            e = __shfl_sync(mask, e, leader);
+        }
         lap(26);
         if (got && e != NONE) {
             const u32 c = e & v.cmask;
@@ -1454,11 +1467,16 @@ __device__ __forceinline__ void cq_alloc(const ouro_heap_view& v, u32 k, u32 gm,
             }
             __syncwarp(mask);
             q_enqueue<FL>(v, k, mask, lane, (ppc - take > 0) ? (1u << leader) : 0u, q_entry(v, c, gen));
+            skip_class = ppc == take;
             if (intodo && rank < take) {
                 *res = v.base + ((u64)c << v.chunk_shift) + ((u64)rank << (v.min_shift + k));
                 *st = OURO_OK;
             }
             todo &= ~__ballot_sync(mask, intodo && rank < take);
+            continue;
+        }
+        if (skip_class) {  // the pool ran dry: the class queue first, then the retry rounds
+            skip_class = false;
             continue;
         }
         // both empty: failed rounds on the leader alone until a poll sees work
