@@ -150,8 +150,6 @@ __device__ __forceinline__ void backoff_policy(u32 policy, u32 base_ns, u32 cap_
     } else {
 #if OURO_FENCE_SCOPE_GPU
         asm volatile("fence.sc.gpu;" ::: "memory");
-#elif OURO_FENCE_NONE
-        // measurement builds only: no fence between rounds
 #else
         asm volatile("fence.sc.cta;" ::: "memory");
 #endif
